@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the batched PBE finite-volume march (BASELINE.json metric: bin-updates/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c4|c3|c2|c1]
+                  [--impl ours|reference]
+
+A bench "step" is one pass of the whole hot path (rows a1-a8: the complete time-march of
+every simulation of this rank's batch, one pbe_run_batch) over one batch of synthetic
+input.  Default workload = BASELINE config 5 (the one the metric is quoted on at
+1/2/4/8 GPUs): 4096 kinetic parameter sets PER GPU (weak scaling: the global ensemble is
+4096 N sims, sharded round-robin), 2000 bins, 8 forward-mode tangent lanes, 600 samples.
+
+One JSON line on rank 0 (see DESIGN.md "Measurement" for every field's definition):
+  value      bin-updates/s over all ranks, inputs resident in HBM, CUDA events on the
+             launch stream, L2 flushed (512 MiB write) between timed iterations
+  e2e        the same metric through the C ABI with pinned HOST buffers: the H2D copy of
+             each step's inputs and the D2H read of its records (moments, status, steps,
+             loss, gradient) inside the timed region
+  roofline   the dominant kernel (k_resident: the only kernel of the step) against the FP64
+             FMA peak (bound "alu"), or HBM for the streaming workload (bound "hbm")
+  cpu_baseline   the CPU oracle timed on a bounded sample on this host's cores
+  --impl reference   the CPU oracle as the reference arm (the paper ships no code)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "bin-updates/sec (bins x steps x sims)"
+UNIT = "bin-updates/s"
+
+
+# ----------------------------------------------------------------------------------------
+# workloads
+# ----------------------------------------------------------------------------------------
+def make_workload(name: str, world: int, args):
+    """The GLOBAL workload (all ranks) and a short description for config."""
+    if name == "c5":
+        w = W.c5_ensemble(n_sims=4096 * world)
+        desc = dict(workload="C5 ensemble + forward-mode tangents", sims_per_gpu=4096, global_sims=4096 * world,
+                    bins=2000, tangent_lanes=8, samples=600, t_max_min=600.0, dt_max=0.05, law="polynomial k=8",
+                    limiter="van Leer")
+    elif name == "c4":
+        N = args.bins or 1_000_000
+        b = args.batch or 64
+        w = W.c4_sweep(N, batch=b * world, n_steps=args.march_steps or 1000)
+        desc = dict(workload=f"C4 bin sweep N={N} batch {b}/GPU", sims_per_gpu=b, bins=N,
+                    march_steps=w.n_steps, limiter="van Leer", cfl="uncapped (C = 0.9)")
+    elif name == "c3":
+        w = W.c3_cycling()
+        desc = dict(workload="C3 temperature cycling (single sim; replicas only)", bins=1000, march_steps=100000)
+    elif name == "c2":
+        w = W.c2_dissolution()
+        desc = dict(workload="C2 dissolution (single sim; replicas only)", bins=1000, march_steps=6000)
+    elif name == "c1":
+        w = W.c1_growth(W.LIM_VANLEER, M=1000)
+        desc = dict(workload="C1 growth, constant G (single sim; replicas only)", bins=100, march_steps=1000)
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return w, desc
+
+
+def replicate_single(w, world: int):
+    """Single-simulation configs run as independent replicas (one per rank)."""
+    return w.subset(np.zeros(world, dtype=np.int64)) if w.n_sims == 1 else w
+
+
+# FP64 flops per bin-update of the method: FMA = 2, div = 1.
+def flops_per_bin_update(limiter: int, P: int) -> float:
+    if limiter == W.LIM_UPWIND:
+        primal = 5.0          # F = C n_up (1), update (2), mu3 FMA (2)
+        lane = 9.0            # Fdot = Cdot n_up + C ndot_up (3), update (2), mu3dot (2), ... (2 for d-free form)
+        return primal + lane * P
+    primal = 12.0             # d (1), psi = 2ab/(a+b) (4), F = C n_up + kap psi (3), update (2), mu3 (2)
+    face_t = 8.0 if P else 0  # psi partials pa, pb (6) + g = n_up + beta psi (2), once per face
+    lane = 13.0               # ddot (1), pa adot + pb bdot (3), Fdot (5), update (2), mu3dot (2)
+    return primal + face_t + lane * P
+
+
+# ----------------------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return dict(sm_mhz=float(np.median(sm)) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                    reasons=reasons, samples=len(rows))
+
+
+# ----------------------------------------------------------------------------------------
+# CPU oracle legs
+# ----------------------------------------------------------------------------------------
+def oracle_sample(w, threads: int, seed_offset: int = 0):
+    """A bounded sample of the workload: `threads` simulations (one per host thread),
+    spread over the batch, full size.  Returns (bin_updates, seconds, description)."""
+    import oracle
+    S = w.n_sims
+    k = min(threads, S)
+    sims = (np.arange(k) * max(S // k, 1) + seed_offset) % S
+    ws = w.subset(sims)
+    mode = oracle.MODE_DUAL if w.n_tangents else oracle.MODE_DOUBLE
+    t0 = time.perf_counter()
+    r = oracle.run(ws, mode=mode, threads=threads, want_n=False)
+    dt = time.perf_counter() - t0
+    bu = float(w.N) * float(np.sum(r["steps"]))
+    desc = f"{k} of {S} sims (full size: {w.N} bins, {w.n_tangents} tangent lanes), one per host thread"
+    return bu, dt, desc
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on this host's cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    w, desc = make_workload(args.workload, 1, args)
+    w = replicate_single(w, 1)
+    th = host_threads()
+    for i in range(args.warmup):
+        oracle_sample(w, th, seed_offset=i)
+    tot_bu, tot_s, sdesc = 0.0, 0.0, ""
+    for i in range(args.steps):
+        bu, s, sdesc = oracle_sample(w, th, seed_offset=args.warmup + i)
+        tot_bu += bu; tot_s += s
+    value = tot_bu / tot_s
+    line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=1e3 * tot_s / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f64", data="synthetic", impl="reference", config=desc,
+                cpu_baseline=dict(value=value, unit=UNIT, cores=th, kind="oracle", sample=sdesc),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                gpu_launches=0)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bins", type=int, default=0, help="C4: bins per simulation")
+    ap.add_argument("--batch", type=int, default=0, help="C4: simulations per GPU")
+    ap.add_argument("--march-steps", type=int, default=0, help="C4: time steps per simulation")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    if "WORLD_SIZE" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2411_00742_b200 as pb
+    from paper_2411_00742_b200 import dist as D
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    wg, desc = make_workload(args.workload, world, args)
+    wg = replicate_single(wg, world)
+    mine = D.shard(wg.n_sims, rank, world)
+    w = wg.subset(mine)
+    P = w.n_tangents
+    ctx = pb.context_for(w, device=local_rank)
+    n0_dev = torch.from_numpy(np.ascontiguousarray(w.n0)).to(dev)
+    ts = w.t_samples if w.n_steps == 0 else None
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ctx.run_batch(n0_dev, w.c0, ts, w.target, stream=stream)
+        if world > 1:
+            out = ctx.moments(on_device=True)
+            grad = ctx.tangents(on_device=True, out=dict(grad=torch.empty((w.n_sims, P), dtype=torch.float64,
+                                                                          device=dev)))["grad"] if P else None
+            rec = D.pack_records(out["status"], out["steps"], out["moments"], out["loss"], grad)
+            D.allgather_records(rec, wg.n_sims)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- warm-up ----------------------------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    res = ctx.moments()
+    steps_local = int(np.sum(res["steps"]))
+    assert np.all(res["status"] == 0), f"simulation failures: {np.unique(res['status'])}"
+    bu_local = float(w.N) * steps_local
+
+    # ---- timed region -------------------------------------------------------------------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    kernel_ms = []
+    for k in range(args.steps):
+        flush.fill_(float(k))                                  # evict L2 between timed iterations
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+        if world == 1:
+            torch.cuda.synchronize(dev)
+            kernel_ms.append(ctx.last_run_info()["main_ms"])
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms, bu_local], dtype=torch.float64, device=dev)
+        mx = t.clone(); dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        sm = t.clone(); dist.all_reduce(sm[1:], op=dist.ReduceOp.SUM)
+        ms, bu_total = float(mx[0]), float(sm[1])
+    else:
+        bu_total = bu_local
+    info = ctx.last_run_info()
+    value = bu_total / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel ----------------------------------------------------------
+    if not kernel_ms:
+        ctx.run_batch(n0_dev, w.c0, ts, w.target, stream=stream)
+        ctx.moments()
+        kernel_ms = [ctx.last_run_info()["main_ms"]]
+    kms = float(np.mean(kernel_ms))
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    mb = None
+    try:
+        import ctypes as C
+        mbl = C.CDLL(os.path.join(ROOT, "paper_2411_00742_b200", "libpbe_mb.so"))
+        mbl.pbe_mb_dfma_tflops.restype = C.c_double
+        mb = float(mbl.pbe_mb_dfma_tflops(local_rank, 5))
+    except Exception:
+        mb = None
+    if info["kernel"] == pb.KERNEL_STREAM:
+        bytes_per = 16.0 * (1 + P)
+        achieved = bytes_per * bu_local / (kms * 1e-3) / 1e9
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        roof = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm, traffic=None,
+                    kernel="k_stream", peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s")
+    else:
+        f = flops_per_bin_update(w.limiter, P)
+        achieved = f * bu_local / (kms * 1e-3) / 1e12
+        peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12     # FP64 FMA lanes x SMs x 2 flops x max SM clock
+        roof = dict(bound="alu", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak, traffic=None,
+                    kernel="k_resident", flops_per_bin_update=f,
+                    peak_source=f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {sm_max:.0f} MHz",
+                    dfma_microbench_tflops=mb, kernel_ms=kms)
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            tr = json.load(open(prof)).get(args.workload)
+            if tr:
+                roof["traffic"] = tr
+        except Exception:
+            pass
+
+    # ---- e2e through the C ABI with pinned host buffers ------------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        n0_h, c0_h = pin(w.n0), pin(w.c0)
+        ts_h = pin(ts) if ts is not None else None
+        tg_h = pin(w.target) if w.target is not None else None
+        S, M = w.n_sims, w.M
+        outh = dict(moments=torch.empty((S, M, 6), dtype=torch.float64).pin_memory().numpy(),
+                    status=torch.empty(S, dtype=torch.int32).pin_memory().numpy(),
+                    steps=torch.empty(S, dtype=torch.int64).pin_memory().numpy(),
+                    loss=torch.empty(S, dtype=torch.float64).pin_memory().numpy())
+        grad_h = torch.empty((S, max(P, 1)), dtype=torch.float64).pin_memory().numpy()
+        h2d = n0_h.nbytes + c0_h.nbytes + (ts_h.nbytes if ts_h is not None else 0) + (tg_h.nbytes if tg_h is not None else 0)
+        d2h = sum(v.nbytes for v in outh.values()) + (S * P * 8 if P else 0)
+
+        def e2e_step():
+            ctx.run_batch(n0_h, c0_h, ts_h, tg_h, stream=stream)
+            ctx.moments(out=outh)
+            if P:
+                ctx.tangents(out=dict(grad=grad_h))
+        e2e_step()
+        barrier(); torch.cuda.synchronize(dev)
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ev2[k][0].record(stream)
+            e2e_step()
+            ev2[k][1].record(stream)
+        torch.cuda.synchronize(dev); barrier()
+        ms2 = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms2], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms2 = float(t[0])
+        e2e = dict(value=bu_total / (ms2 * 1e-3), unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                   ms_per_step=ms2, host_buffers="pinned", api="C ABI pbe_run_batch(n0_on_device=0) + pbe_moments")
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        th = host_threads()
+        bu, s, sdesc = oracle_sample(w, th)
+        cpu = dict(value=bu / s, unit=UNIT, cores=th, kind="oracle", sample=sdesc, seconds=s)
+
+    if rank == 0:
+        cfg = dict(desc)
+        cfg.update(parallelism=f"sims sharded round-robin over {world} GPU(s); NCCL allgather of per-sim records"
+                   if world > 1 else "1 GPU", l2="flushed between timed iterations (512 MiB write)",
+                   steps_per_sim_mean=steps_local / max(w.n_sims, 1), kernel=info)
+        line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+                    ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                    data="synthetic (seeded; DESIGN.md input recipe)", config=cfg, roofline=roof,
+                    cpu_baseline=cpu, e2e=e2e, gpu_launches=int(info["launches"]) * args.steps, clocks=clk)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,390 @@
+// =====================================================================================
+//  pbe_api.cu — host side of libpbe: the C ABI declared in include/pbe.h.
+//  Validation, context-owned device memory, stream-ordered launches, kernel dispatch
+//  by (N, tangent lanes).  No computation of the method happens here: every step of
+//  the march runs in the CUDA kernels (k_resident.cuh, k_stream.cuh, k_cluster.cuh).
+// =====================================================================================
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pbe.h"
+#include "pbe_device.cuh"
+#include "k_resident.cuh"
+
+using pbe::KParams;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t b) {
+        if (b <= bytes && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr; bytes = 0;
+        if (b == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct pbe_ctx_s {
+    pbe_config cfg{};
+    int device = 0;
+    std::string err;
+    // kinetics
+    bool have_kin = false;
+    int law = 0, n_params = 0, kin_sims = 0, sol_kind = 0, n_sol = 0, n_knots = 0;
+    bool knotT_per_sim = false;
+    DevBuf theta, sol, knot_t, knot_T, seed;
+    // run inputs
+    DevBuf c0, tsamp, target, n0_staged;
+    // outputs
+    DevBuf rec, trec, status, steps, loss, grad;
+    // last run
+    bool have_run = false;
+    int last_sims = 0;
+    cudaStream_t last_stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    pbe_run_info info{};
+};
+
+static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf; else g_create_error = buf;
+    return st;
+}
+
+#define CUDA_TRY(ctx, call)                                                                  \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? PBE_ERR_NOMEM : PBE_ERR_CUDA, \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+// ------------------------------------------------------------------------------------
+// Kernel dispatch table for k_resident<P, K, MAXT>
+// ------------------------------------------------------------------------------------
+namespace {
+
+using KernelFn = void (*)(const KParams);
+
+struct ResidentVariant {
+    int P, K, maxt;
+    KernelFn fn;
+};
+size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)4 * (1 + v.P) * nt * sizeof(double); }
+
+#define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
+const ResidentVariant kResident[] = {
+    RV(0, 2, 512),  RV(0, 4, 512),  RV(0, 8, 512),  RV(0, 16, 512),
+    RV(2, 2, 512),  RV(2, 4, 512),  RV(2, 8, 512),  RV(2, 16, 256),
+    RV(4, 2, 512),  RV(4, 4, 512),  RV(4, 8, 256),
+    RV(8, 2, 256),  RV(8, 4, 256),  RV(8, 8, 256),
+    RV(10, 2, 256), RV(10, 4, 256),
+};
+#undef RV
+
+int lanes_instantiated(int P) {
+    if (P == 0) return 0;
+    if (P <= 2) return 2;
+    if (P <= 4) return 4;
+    if (P <= 8) return 8;
+    return 10;
+}
+
+// smallest K (fewest registers per thread) whose CTA covers N bins
+const ResidentVariant* pick_resident(int N, int P) {
+    const int Pi = lanes_instantiated(P);
+    const ResidentVariant* best = nullptr;
+    for (const auto& v : kResident) {
+        if (v.P != Pi) continue;
+        if ((long long)v.K * v.maxt < N) continue;
+        if (!best || v.K < best->K) best = &v;
+    }
+    return best;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------
+extern "C" {
+
+const char* pbe_version(void) { return "libpbe 0.1 (sm_100a)"; }
+
+const char* pbe_last_error(pbe_ctx ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
+    if (!cfg || !out) return fail(nullptr, PBE_ERR_ARG, "pbe_create: NULL cfg or out");
+    *out = nullptr;
+    const pbe_config& c = *cfg;
+    if (c.n_bins < 3) return fail(nullptr, PBE_ERR_ARG, "n_bins must be >= 3 (got %d)", c.n_bins);
+    if (!(c.dL > 0.0) || !std::isfinite(c.dL)) return fail(nullptr, PBE_ERR_ARG, "dL must be finite and > 0");
+    if (!std::isfinite(c.L_lo)) return fail(nullptr, PBE_ERR_ARG, "L_lo must be finite");
+    if (c.limiter != PBE_LIM_UPWIND && c.limiter != PBE_LIM_VANLEER)
+        return fail(nullptr, PBE_ERR_ARG, "unknown limiter %d", c.limiter);
+    if (!(c.courant > 0.0 && c.courant <= 1.0)) return fail(nullptr, PBE_ERR_ARG, "courant must be in (0, 1]");
+    if (!(c.dt_fixed >= 0.0) || !std::isfinite(c.dt_fixed)) return fail(nullptr, PBE_ERR_ARG, "dt_fixed must be >= 0");
+    if (!(c.dt_max > 0.0)) return fail(nullptr, PBE_ERR_ARG, "dt_max must be > 0 (INFINITY for no cap)");
+    if (c.max_steps <= 0) return fail(nullptr, PBE_ERR_ARG, "max_steps must be > 0");
+    if (c.n_steps < 0) return fail(nullptr, PBE_ERR_ARG, "n_steps must be >= 0");
+    if (!(c.rho_c > 0.0) || !(c.k_v > 0.0)) return fail(nullptr, PBE_ERR_ARG, "rho_c and k_v must be > 0");
+    if (c.n_samples < 1) return fail(nullptr, PBE_ERR_ARG, "n_samples must be >= 1");
+    if (c.n_steps > 0 && c.n_samples != 1) return fail(nullptr, PBE_ERR_ARG, "steps mode needs n_samples == 1");
+    if (c.n_tangents < 0 || c.n_tangents > pbe::MAXP) return fail(nullptr, PBE_ERR_ARG, "n_tangents must be in [0, 10]");
+    if (c.max_sims < 1) return fail(nullptr, PBE_ERR_ARG, "max_sims must be >= 1");
+    if (c.kernel < PBE_KERNEL_AUTO || c.kernel > PBE_KERNEL_STREAM) return fail(nullptr, PBE_ERR_ARG, "unknown kernel %d", c.kernel);
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(nullptr, PBE_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(nullptr, PBE_ERR_ARG, "device %d out of range [0, %d)", device, ndev);
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(nullptr, PBE_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+
+    pbe_ctx ctx = new pbe_ctx_s();
+    ctx->cfg = c;
+    ctx->device = device;
+    const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
+    cudaError_t ea = cudaSuccess;
+    if (ea == cudaSuccess) ea = ctx->rec.ensure(S * M * 6 * sizeof(double));
+    if (ea == cudaSuccess) ea = ctx->trec.ensure(S * M * (P ? P : 1) * 5 * sizeof(double));
+    if (ea == cudaSuccess) ea = ctx->status.ensure(S * sizeof(int));
+    if (ea == cudaSuccess) ea = ctx->steps.ensure(S * sizeof(long long));
+    if (ea == cudaSuccess) ea = ctx->loss.ensure(S * sizeof(double));
+    if (ea == cudaSuccess) ea = ctx->grad.ensure(S * (P ? P : 1) * sizeof(double));
+    if (ea == cudaSuccess) ea = ctx->c0.ensure(S * sizeof(double));
+    if (ea == cudaSuccess) ea = ctx->tsamp.ensure(M * sizeof(double));
+    if (ea == cudaSuccess) ea = cudaEventCreate(&ctx->ev0);
+    if (ea == cudaSuccess) ea = cudaEventCreate(&ctx->ev1);
+    if (ea != cudaSuccess) {
+        const pbe_status st = ea == cudaErrorMemoryAllocation ? PBE_ERR_NOMEM : PBE_ERR_CUDA;
+        fail(nullptr, st, "pbe_create: %s", cudaGetErrorString(ea));
+        pbe_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return PBE_OK;
+}
+
+void pbe_destroy(pbe_ctx ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (DevBuf* b : {&ctx->theta, &ctx->sol, &ctx->knot_t, &ctx->knot_T, &ctx->seed, &ctx->c0, &ctx->tsamp,
+                      &ctx->target, &ctx->n0_staged, &ctx->rec, &ctx->trec, &ctx->status, &ctx->steps,
+                      &ctx->loss, &ctx->grad})
+        b->release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    delete ctx;
+}
+
+pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t n_sims, const double* theta,
+                            int32_t sol_kind, int32_t n_sol, const double* sol_params, int32_t n_knots,
+                            const double* knot_t, const double* knot_T, int32_t knot_T_per_sim,
+                            const double* tangent_seed) {
+    if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
+    if (law < PBE_LAW_CONST || law > PBE_LAW_POLY) return fail(ctx, PBE_ERR_ARG, "unknown law %d", law);
+    if (n_params < 1 || n_params > pbe::MAXTH) return fail(ctx, PBE_ERR_ARG, "n_params must be in [1, 10]");
+    if (law == PBE_LAW_CONST && n_params != 1) return fail(ctx, PBE_ERR_ARG, "PBE_LAW_CONST takes 1 parameter");
+    if (law == PBE_LAW_ARRHENIUS_GD && n_params != 3 && n_params != 6)
+        return fail(ctx, PBE_ERR_ARG, "PBE_LAW_ARRHENIUS_GD takes 3 or 6 parameters");
+    if (n_sims < 1 || n_sims > ctx->cfg.max_sims) return fail(ctx, PBE_ERR_ARG, "n_sims must be in [1, max_sims]");
+    if (!theta || !sol_params || !knot_t || !knot_T) return fail(ctx, PBE_ERR_ARG, "NULL kinetics array");
+    if (sol_kind == PBE_SOL_EXP ? n_sol != 2 : (sol_kind == PBE_SOL_POLY ? n_sol != 3 : true))
+        return fail(ctx, PBE_ERR_ARG, "solubility: EXP takes 2 parameters, POLY takes 3");
+    if (n_knots < 1) return fail(ctx, PBE_ERR_ARG, "n_knots must be >= 1");
+    for (int k = 1; k < n_knots; ++k)
+        if (!(knot_t[k] > knot_t[k - 1])) return fail(ctx, PBE_ERR_ARG, "knot_t must be strictly increasing");
+    const size_t nth = (size_t)n_sims * n_params;
+    for (size_t j = 0; j < nth; ++j)
+        if (!std::isfinite(theta[j])) return fail(ctx, PBE_ERR_ARG, "theta[%zu] is not finite", j);
+    const size_t nT = (size_t)(knot_T_per_sim ? n_sims : 1) * n_knots;
+    for (size_t j = 0; j < nT; ++j)
+        if (!std::isfinite(knot_T[j])) return fail(ctx, PBE_ERR_ARG, "knot_T[%zu] is not finite", j);
+    const int P = ctx->cfg.n_tangents, nsd = n_params + n_sol;
+    std::vector<double> seed((size_t)(P ? P : 1) * nsd, 0.0);
+    if (tangent_seed) std::memcpy(seed.data(), tangent_seed, (size_t)P * nsd * sizeof(double));
+    else for (int p = 0; p < P && p < n_params; ++p) seed[(size_t)p * nsd + p] = 1.0;
+
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    CUDA_TRY(ctx, ctx->theta.ensure(nth * sizeof(double)));
+    CUDA_TRY(ctx, ctx->sol.ensure(3 * sizeof(double)));
+    CUDA_TRY(ctx, ctx->knot_t.ensure(n_knots * sizeof(double)));
+    CUDA_TRY(ctx, ctx->knot_T.ensure(nT * sizeof(double)));
+    CUDA_TRY(ctx, ctx->seed.ensure(seed.size() * sizeof(double)));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->theta.p, theta, nth * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->sol.p, sol_params, n_sol * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->knot_t.p, knot_t, n_knots * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->knot_T.p, knot_T, nT * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ctx->seed.p, seed.data(), seed.size() * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->law = law; ctx->n_params = n_params; ctx->kin_sims = n_sims; ctx->sol_kind = sol_kind;
+    ctx->n_sol = n_sol; ctx->n_knots = n_knots; ctx->knotT_per_sim = knot_T_per_sim != 0;
+    ctx->have_kin = true;
+    return PBE_OK;
+}
+
+pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride, int32_t n0_on_device,
+                         const double* c0, const double* t_samples, const double* target, double* n_final,
+                         double* ndot_final, void* cuda_stream) {
+    if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
+    if (!ctx->have_kin) return fail(ctx, PBE_ERR_STATE, "pbe_set_kinetics must precede pbe_run_batch");
+    const pbe_config& cf = ctx->cfg;
+    const int N = cf.n_bins, M = cf.n_samples, P = cf.n_tangents;
+    const bool steps_mode = cf.n_steps > 0;
+    if (n_sims < 1 || n_sims > cf.max_sims) return fail(ctx, PBE_ERR_ARG, "n_sims must be in [1, max_sims]");
+    if (n_sims != ctx->kin_sims) return fail(ctx, PBE_ERR_ARG, "n_sims (%d) != kinetics n_sims (%d)", n_sims, ctx->kin_sims);
+    if (!n0 || !c0) return fail(ctx, PBE_ERR_ARG, "NULL n0 or c0");
+    if (n0_stride != 0 && n0_stride != N) return fail(ctx, PBE_ERR_ARG, "n0_stride must be 0 or n_bins");
+    if (!steps_mode && !t_samples) return fail(ctx, PBE_ERR_ARG, "NULL t_samples");
+    for (int s = 0; s < n_sims; ++s)
+        if (!(c0[s] >= 0.0) || !std::isfinite(c0[s])) return fail(ctx, PBE_ERR_ARG, "c0[%d] must be finite and >= 0", s);
+    if (!steps_mode) {
+        if (!(t_samples[0] > 0.0)) return fail(ctx, PBE_ERR_ARG, "t_samples[0] must be > 0");
+        for (int m = 1; m < M; ++m)
+            if (!(t_samples[m] > t_samples[m - 1])) return fail(ctx, PBE_ERR_ARG, "t_samples must be strictly increasing");
+        if (!std::isfinite(t_samples[M - 1])) return fail(ctx, PBE_ERR_ARG, "t_samples must be finite");
+    }
+    if (!n0_on_device) {
+        const size_t rows = n0_stride ? (size_t)n_sims : 1;
+        for (size_t j = 0; j < rows * N; ++j)
+            if (!(n0[j] >= 0.0) || !std::isfinite(n0[j])) return fail(ctx, PBE_ERR_ARG, "n0[%zu] must be finite and >= 0", j);
+    }
+    if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
+
+    // kernel choice
+    const ResidentVariant* rv = pick_resident(N, P);
+    int kind = cf.kernel == PBE_KERNEL_AUTO ? PBE_KERNEL_RESIDENT : cf.kernel;
+    if (kind != PBE_KERNEL_RESIDENT)
+        return fail(ctx, PBE_ERR_ARG, "kernel variant %d not available in this build", kind);
+    if (!rv) return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit the resident kernel", N, P);
+
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->c0.p, c0, n_sims * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (!steps_mode)
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->tsamp.p, t_samples, M * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (target) {
+        CUDA_TRY(ctx, ctx->target.ensure((size_t)n_sims * M * 2 * sizeof(double)));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->target.p, target, (size_t)n_sims * M * 2 * sizeof(double),
+                                      cudaMemcpyHostToDevice, st));
+    }
+    const double* n0_dev = n0;
+    if (!n0_on_device) {
+        const size_t bytes = (n0_stride ? (size_t)n_sims : 1) * N * sizeof(double);
+        CUDA_TRY(ctx, ctx->n0_staged.ensure(bytes));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->n0_staged.p, n0, bytes, cudaMemcpyHostToDevice, st));
+        n0_dev = ctx->n0_staged.as<double>();
+    }
+    // unreached samples read as NaN (all-ones bytes)
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->rec.p, 0xff, (size_t)n_sims * M * 6 * sizeof(double), st));
+    if (P) CUDA_TRY(ctx, cudaMemsetAsync(ctx->trec.p, 0xff, (size_t)n_sims * M * P * 5 * sizeof(double), st));
+
+    KParams kp{};
+    kp.N = N; kp.L_lo = cf.L_lo; kp.dL = cf.dL; kp.limiter = cf.limiter;
+    kp.courant = cf.courant; kp.dt_fixed = cf.dt_fixed; kp.dt_max = cf.dt_max;
+    kp.max_steps = cf.max_steps; kp.n_steps = cf.n_steps; kp.rho_kv = cf.rho_c * cf.k_v;
+    kp.law = ctx->law; kp.n_params = ctx->n_params; kp.sol_kind = ctx->sol_kind; kp.n_sol = ctx->n_sol;
+    kp.n_knots = ctx->n_knots; kp.knotT_stride = ctx->knotT_per_sim ? ctx->n_knots : 0;
+    kp.theta = ctx->theta.as<double>(); kp.sol = ctx->sol.as<double>(); kp.knot_t = ctx->knot_t.as<double>();
+    kp.knot_T = ctx->knot_T.as<double>(); kp.seed = ctx->seed.as<double>();
+    kp.n_sims = n_sims; kp.M = M; kp.P = P;
+    kp.n0 = n0_dev; kp.n0_stride = n0_stride; kp.c0 = ctx->c0.as<double>();
+    kp.t_samples = ctx->tsamp.as<double>(); kp.target = target ? ctx->target.as<double>() : nullptr;
+    kp.rec = ctx->rec.as<double>(); kp.trec = ctx->trec.as<double>(); kp.status = ctx->status.as<int>();
+    kp.steps = ctx->steps.as<long long>(); kp.loss = ctx->loss.as<double>(); kp.grad = ctx->grad.as<double>();
+    kp.n_final = n_final; kp.ndot_final = ndot_final;
+
+    const int nt = ((N + rv->K - 1) / rv->K + 31) / 32 * 32;
+    const size_t smem = resident_smem(*rv, nt);
+    CUDA_TRY(ctx, cudaFuncSetAttribute(rv->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    rv->fn<<<n_sims, nt, smem, st>>>(kp);
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+
+    ctx->info = pbe_run_info{};
+    ctx->info.kernel = PBE_KERNEL_RESIDENT;
+    ctx->info.launches = 1;
+    ctx->info.threads_per_cta = nt;
+    ctx->info.ctas = n_sims;
+    ctx->info.cluster = 1;
+    ctx->info.bins_per_thread = rv->K;
+    ctx->info.main_ms = -1.0;
+    ctx->have_run = true;
+    ctx->last_sims = n_sims;
+    ctx->last_stream = st;
+    return PBE_OK;
+}
+
+static pbe_status finish_run(pbe_ctx ctx) {
+    if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
+    if (!ctx->have_run) return fail(ctx, PBE_ERR_STATE, "no run to read (call pbe_run_batch first)");
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->last_stream));
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) ctx->info.main_ms = ms;
+    return PBE_OK;
+}
+
+// D2H/D2D copies are stream-ordered on the run's stream, then the stream is synchronized
+// (so CUDA events recorded on that stream afterwards bracket the copies too).
+static pbe_status copy_out(pbe_ctx ctx, void* dst, const void* src, size_t bytes, int32_t on_device) {
+    if (!dst || bytes == 0) return PBE_OK;
+    CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                  ctx->last_stream));
+    return PBE_OK;
+}
+
+pbe_status pbe_moments(pbe_ctx ctx, double* moments, int32_t* sim_status, int64_t* sim_steps, double* loss,
+                       int32_t on_device) {
+    pbe_status r = finish_run(ctx);
+    if (r != PBE_OK) return r;
+    const size_t S = ctx->last_sims, M = ctx->cfg.n_samples;
+    if ((r = copy_out(ctx, moments, ctx->rec.p, S * M * 6 * sizeof(double), on_device)) != PBE_OK) return r;
+    if ((r = copy_out(ctx, sim_status, ctx->status.p, S * sizeof(int), on_device)) != PBE_OK) return r;
+    if ((r = copy_out(ctx, sim_steps, ctx->steps.p, S * sizeof(long long), on_device)) != PBE_OK) return r;
+    if ((r = copy_out(ctx, loss, ctx->loss.p, S * sizeof(double), on_device)) != PBE_OK) return r;
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->last_stream));
+    return PBE_OK;
+}
+
+pbe_status pbe_tangents(pbe_ctx ctx, double* tangents, double* grad, int32_t on_device) {
+    pbe_status r = finish_run(ctx);
+    if (r != PBE_OK) return r;
+    const size_t S = ctx->last_sims, M = ctx->cfg.n_samples, P = ctx->cfg.n_tangents;
+    if (P == 0) return fail(ctx, PBE_ERR_STATE, "context has no tangent lanes");
+    if ((r = copy_out(ctx, tangents, ctx->trec.p, S * M * P * 5 * sizeof(double), on_device)) != PBE_OK) return r;
+    if ((r = copy_out(ctx, grad, ctx->grad.p, S * P * sizeof(double), on_device)) != PBE_OK) return r;
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->last_stream));
+    return PBE_OK;
+}
+
+pbe_status pbe_last_run_info(pbe_ctx ctx, pbe_run_info* info) {
+    if (!ctx || !info) return fail(ctx, PBE_ERR_ARG, "NULL argument");
+    if (!ctx->have_run) return fail(ctx, PBE_ERR_STATE, "no run yet");
+    *info = ctx->info;
+    return PBE_OK;
+}
+
+}  // extern "C"

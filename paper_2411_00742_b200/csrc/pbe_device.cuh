@@ -1,0 +1,249 @@
+// =====================================================================================
+//  pbe_device.cuh — device-side building blocks shared by the libpbe kernels
+//  (k_resident, k_cluster, k_stream).  sm_100a, FP64 on the SIMT pipes (nothing on the
+//  path is a dense contraction, so no tensor cores).
+//
+//  Contents
+//    KParams        kernel arguments (device pointers + problem constants)
+//    D1             one-lane forward-mode dual number: warp lane p carries tangent p, so
+//                   one warp evaluates the scalar kinetics for all P <= 10 directions at
+//                   once (primal + tangent in one pass)
+//    kinetics       row a1: T(t), c*(T), S = c/c*, G(S, T; theta)   (L285, L693-705, L565-571)
+//    time step      row a2: CFL / dt_max / fixed dt / landing on sample times (R-7..R-9)
+//    limited slope  row a3: psi(a,b) = 2ab/(a+b) for ab > 0, else 0  (= phi_vL(a/b) b)
+//    warp_transpose_reduce   V partial sums over 32 lanes in ~V+5 shuffles
+// =====================================================================================
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pbe {
+
+constexpr int MAXP = 10;   // tangent lanes
+constexpr int MAXTH = 10;  // kinetic parameters
+
+enum { LIM_UPWIND = 0, LIM_VANLEER = 1 };
+enum { LAW_CONST = 0, LAW_ARRH = 1, LAW_POLY = 2 };
+enum { SOL_EXP = 0, SOL_POLY = 1 };
+enum { ST_OK = 0, ST_CFL = 2, ST_NEG = 3, ST_INFEAS = 4, ST_MAXSTEPS = 5 };
+
+struct KParams {
+    // grid and scheme
+    int N;
+    double L_lo, dL;
+    int limiter;
+    double courant, dt_fixed, dt_max;
+    long long max_steps, n_steps;
+    double rho_kv;          // rho_c * k_v
+    // kinetics
+    int law, n_params, sol_kind, n_sol, n_knots;
+    long long knotT_stride; // 0 (shared profile) or n_knots
+    const double* theta;    // [S][n_params]
+    const double* sol;      // [n_sol]
+    const double* knot_t;   // [n_knots]
+    const double* knot_T;   // [S or 1][n_knots]
+    const double* seed;     // [P][n_params + n_sol]
+    // batch
+    int n_sims, M, P;       // P = tangent lanes requested (<= instantiated lanes)
+    const double* n0; long long n0_stride;
+    const double* c0;       // [S]
+    const double* t_samples;// [M]
+    const double* target;   // [S][M][2] or nullptr
+    // outputs
+    double* rec;            // [S][M][6]
+    double* trec;           // [S][M][P][5]
+    int* status;            // [S]
+    long long* steps;       // [S]
+    double* loss;           // [S]
+    double* grad;           // [S][P]
+    double* n_final;        // [S][N] or nullptr
+    double* ndot_final;     // [S][P][N] or nullptr
+};
+
+// ------------------------------------------------------------------------------------
+// D1: value + one tangent (this lane's direction)
+// ------------------------------------------------------------------------------------
+struct D1 { double v, d; };
+__device__ __forceinline__ D1 mk(double v, double d = 0.0) { return D1{v, d}; }
+__device__ __forceinline__ D1 operator+(D1 a, D1 b) { return {a.v + b.v, a.d + b.d}; }
+__device__ __forceinline__ D1 operator-(D1 a, D1 b) { return {a.v - b.v, a.d - b.d}; }
+__device__ __forceinline__ D1 operator-(D1 a) { return {-a.v, -a.d}; }
+__device__ __forceinline__ D1 operator*(D1 a, D1 b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+__device__ __forceinline__ D1 operator/(D1 a, D1 b) { const double q = a.v / b.v; return {q, (a.d - q * b.d) / b.v}; }
+__device__ __forceinline__ D1 operator+(D1 a, double b) { return {a.v + b, a.d}; }
+__device__ __forceinline__ D1 operator-(D1 a, double b) { return {a.v - b, a.d}; }
+__device__ __forceinline__ D1 operator+(double a, D1 b) { return {a + b.v, b.d}; }
+__device__ __forceinline__ D1 operator-(double a, D1 b) { return {a - b.v, -b.d}; }
+__device__ __forceinline__ D1 operator*(D1 a, double b) { return {a.v * b, a.d * b}; }
+__device__ __forceinline__ D1 operator*(double a, D1 b) { return {a * b.v, a * b.d}; }
+__device__ __forceinline__ D1 operator/(D1 a, double b) { return {a.v / b, a.d / b}; }
+__device__ __forceinline__ D1 operator/(double a, D1 b) { const double q = a / b.v; return {q, -q * b.d / b.v}; }
+__device__ __forceinline__ D1 dexp(D1 a) { const double e = exp(a.v); return {e, e * a.d}; }
+__device__ __forceinline__ D1 dlog(D1 a) { return {log(a.v), a.d / a.v}; }
+// |x| with d|x| = sgn(x) dx, sgn(0) = 0 (R-20)
+__device__ __forceinline__ D1 dabs(D1 a) { return a.v > 0.0 ? a : (a.v < 0.0 ? -a : D1{0.0, 0.0}); }
+
+// ------------------------------------------------------------------------------------
+// Row a1: kinetics.  `th`/`so` hold theta and solubility parameters as D1 (this lane's
+// seed), `kT` points at this simulation's temperature knots.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ D1 temperature(const KParams& kp, const double* __restrict__ kT, D1 t) {
+    const int K = kp.n_knots;
+    if (K == 1 || t.v <= kp.knot_t[0]) return mk(kT[0]);
+    if (t.v >= kp.knot_t[K - 1]) return mk(kT[K - 1]);
+    int k = 0;
+    while (!(t.v >= kp.knot_t[k] && t.v < kp.knot_t[k + 1])) ++k;
+    const double slope = (kT[k + 1] - kT[k]) / (kp.knot_t[k + 1] - kp.knot_t[k]);
+    return kT[k] + slope * (t - kp.knot_t[k]);
+}
+
+// Parameters are read on demand through a loader (this lane's seed) so no D1 array of
+// theta has to live in registers next to the resident state.
+struct KinLoader {
+    const double* th;     // this simulation's theta
+    const double* sol;    // solubility parameters
+    const double* seed;   // [P][n_params + n_sol]
+    int lane_p;           // tangent lane of this thread (-1: none)
+    int n_params, nsd;
+    __device__ __forceinline__ D1 theta(int j) const {
+        return mk(__ldg(th + j), lane_p >= 0 ? __ldg(seed + lane_p * nsd + j) : 0.0);
+    }
+    __device__ __forceinline__ D1 so(int j) const {
+        return mk(__ldg(sol + j), lane_p >= 0 ? __ldg(seed + lane_p * nsd + n_params + j) : 0.0);
+    }
+};
+
+__device__ __forceinline__ D1 solubility(const KParams& kp, const KinLoader& L, D1 T) {
+    if (kp.sol_kind == SOL_EXP) return L.so(0) * dexp(L.so(1) * T);          // Eq. A.1
+    return L.so(0) + L.so(1) * T + L.so(2) * T * T;                           // R-13
+}
+
+__device__ __forceinline__ D1 dpow(D1 x, D1 y) { return dexp(y * dlog(x)); }   // R-18
+
+__device__ __forceinline__ D1 growth_rate(const KParams& kp, const KinLoader& L, D1 S, D1 T) {
+    if (kp.law == LAW_CONST) return L.theta(0);
+    if (kp.law == LAW_ARRH) {
+        if (S.v > 1.0)                                                                 // Eq. A.2
+            return L.theta(0) * dexp(-L.theta(1) / (T + 273.15)) * dpow(S - 1.0, L.theta(2));
+        if (S.v < 1.0 && kp.n_params >= 6)                                             // R-12
+            return -(L.theta(3) * dexp(-L.theta(4) / (T + 273.15)) * dpow(1.0 - S, L.theta(5)));
+        return mk(0.0);
+    }
+    if (S.v > 1.0) {                                                      // eq-poly_growth_rate
+        const D1 x = S - 1.0;
+        D1 g = mk(0.0), xp = x;
+        for (int j = 0; j < kp.n_params; ++j) { g = g + L.theta(j) * xp; xp = xp * x; }
+        return g;
+    }
+    return mk(0.0);
+}
+
+// Per-step scalars produced by the kinetics warp and consumed by every thread.
+struct StepScalars {
+    D1 C;        // Courant number G dt / dL (+ this lane's tangent)
+    D1 kap;      // 1/2 |C| (1 - |C|)
+    D1 dt;       // time step
+    bool landing;
+    int err;     // ST_CFL if fixed-dt |C| > 1
+};
+
+// Row a2: the time step at (t, G) toward sample time tn (R-7, R-8, R-9).
+__device__ __forceinline__ StepScalars time_step(const KParams& kp, D1 G, D1 t, double tn, bool steps_mode) {
+    StepScalars r;
+    r.landing = false; r.err = ST_OK;
+    D1 dt, C;
+    if (kp.dt_fixed > 0.0) {
+        dt = mk(kp.dt_fixed);
+        C = G * dt / kp.dL;
+        if (fabs(C.v) > 1.0) r.err = ST_CFL;
+    } else if (G.v != 0.0) {
+        const D1 dt_cfl = (kp.courant * kp.dL) / dabs(G);
+        if (kp.dt_max < dt_cfl.v) { dt = mk(kp.dt_max); C = G * dt / kp.dL; }
+        else { dt = dt_cfl; C = mk(G.v > 0.0 ? kp.courant : -kp.courant); }   // C = nu sgn G (R-9)
+    } else {
+        dt = mk(kp.dt_max);
+        C = mk(0.0);
+    }
+    if (!steps_mode) {
+        if (t.v + dt.v >= tn - 1e-9 * dt.v) {
+            const D1 dtl = tn - t;
+            const D1 Cl = G * dtl / kp.dL;
+            if (fabs(Cl.v) <= 1.0) { dt = dtl; C = Cl; r.landing = true; }
+        }
+    } else if (isinf(dt.v)) {
+        dt = mk(0.0);
+    }
+    const D1 aC = dabs(C);
+    r.C = C; r.dt = dt;
+    r.kap = 0.5 * aC * (1.0 - aC);
+    return r;
+}
+
+// ------------------------------------------------------------------------------------
+// Row a3: limited slope psi(a, b) = phi_vanLeer(a/b) * b = 2ab/(a+b) (ab > 0), else 0,
+// plus the partials pa = d psi/da = 2 (b/(a+b))^2 and pb = 2 (a/(a+b))^2 for tangents.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double psi_vl(double a, double b) {
+    return (a * b > 0.0) ? (2.0 * a * b) / (a + b) : 0.0;
+}
+__device__ __forceinline__ void psi_vl_d(double a, double b, double& psi, double& pa, double& pb) {
+    if (a * b > 0.0) {
+        const double r = 1.0 / (a + b);
+        const double br = b * r, ar = a * r;
+        psi = 2.0 * a * br;
+        pa = 2.0 * br * br;
+        pb = 2.0 * ar * ar;
+    } else {
+        psi = 0.0; pa = 0.0; pb = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Transpose-reduce V per-lane values across a warp in ~V + 5 FP64 shuffles (instead of
+// 5 V): each level halves the list a lane keeps.  On exit, lane l holds in v[0] the warp
+// total of value index reduce_index<V>(l) (values >= V are padding).
+// ------------------------------------------------------------------------------------
+template <int V> struct RLevels {
+    // list sizes per level: V, ceil(V/2), ...  (up to 5 levels, bits 4..0)
+    __host__ __device__ static constexpr int n(int lvl) { return lvl == 0 ? V : (n(lvl - 1) + 1) / 2; }
+};
+
+template <int V>
+__device__ __forceinline__ int reduce_index(int lane) {
+    // position in the original list; returns V (= padding) when the lane's final slot is
+    // a pad entry of a shorter upper half
+    int idx = 0, real = V;
+#pragma unroll
+    for (int lvl = 0; lvl < 5; ++lvl) {
+        const int n = RLevels<V>::n(lvl);
+        if (n <= 1) break;
+        const int h = (n + 1) / 2;
+        if (lane & (16 >> lvl)) { idx += h; real -= h; }
+        else if (real > h) real = h;
+    }
+    return real >= 1 ? idx : V;
+}
+
+template <int V>
+__device__ __forceinline__ void warp_transpose_reduce(double (&v)[V], int lane) {
+#pragma unroll
+    for (int lvl = 0; lvl < 5; ++lvl) {
+        const int off = 16 >> lvl;
+        const int n = RLevels<V>::n(lvl);
+        if (n > 1) {
+            const int h = (n + 1) / 2;
+            const bool hi = (lane & off) != 0;
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const double upper = (h + j < n) ? v[(h + j < V) ? h + j : 0] : 0.0;
+                const double send = hi ? v[j] : upper;
+                const double keep = hi ? upper : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+        }
+    }
+}
+
+}  // namespace pbe

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Tolerances (BASELINE.json north star):
+    moments and concentration   1e-10 relative
+    distribution n              1e-9 * max(n)
+    tangent records / ndot      1e-8 * max |lane|     (R-21: per lane)
+    loss / gradient             1e-9 relative
+Integers (status, step counts) must match exactly."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+RTOL_MOM = 1e-10
+RTOL_N = 1e-9
+RTOL_TAN = 1e-8
+
+
+def _gpu(w, **kw):
+    import paper_2411_00742_b200 as pb
+    return pb.run_workload(w, **kw)
+
+
+def _cmp_samples(g, o, rtol=RTOL_MOM):
+    a, b = g["samples"], o["samples"]
+    assert a.shape == b.shape
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    ok = ~np.isnan(b)
+    err = np.abs(a[ok] - b[ok]) / np.maximum(np.abs(b[ok]), 1e-300)
+    # time stamps and moments: relative; mu0's tiny drift terms are compared relative to mu0
+    assert err.max() <= rtol, f"max rel err {err.max():.3e}"
+
+
+def _cmp_n(g, o, rtol=RTOL_N):
+    for s in range(o["n_final"].shape[0]):
+        scale = np.max(np.abs(o["n_final"][s]))
+        assert np.max(np.abs(g["n_final"][s] - o["n_final"][s])) <= rtol * scale
+
+
+def _cmp_tangents(g, o, rtol=RTOL_TAN):
+    a, b = g["tsamples"], o["tsamples"]
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    S, M, P, _ = b.shape
+    for s in range(S):
+        for p in range(P):
+            for k in range(5):
+                x, y = a[s, :, p, k], b[s, :, p, k]
+                ok = ~np.isnan(y)
+                if not ok.any():
+                    continue
+                scale = np.max(np.abs(y[ok]))
+                if scale == 0:
+                    assert np.all(x[ok] == 0)
+                    continue
+                if k == 1:   # d mu0: exactly 0 without boundary flux, rounding-level otherwise
+                    scale = max(scale, 1e-6 * np.max(np.abs(b[s, :, p, 2][ok])) / 400.0)
+                assert np.max(np.abs(x[ok] - y[ok])) <= rtol * scale, (s, p, k)
+
+
+def _check(w, mode=oracle.MODE_DOUBLE, **kw):
+    o = oracle.run(w, mode=mode, threads=8)
+    g = _gpu(w, **kw)
+    assert np.array_equal(g["status"], o["status"]), (g["status"], o["status"])
+    assert np.array_equal(g["steps"], o["steps"]), (g["steps"], o["steps"])
+    _cmp_samples(g, o)
+    _cmp_n(g, o)
+    if mode != oracle.MODE_DOUBLE:
+        _cmp_tangents(g, o)
+        for s in range(w.n_sims):
+            for p in range(w.n_tangents):
+                sc = np.max(np.abs(o["ndot_final"][s, p]))
+                assert np.max(np.abs(g["ndot_final"][s, p] - o["ndot_final"][s, p])) <= RTOL_TAN * max(sc, 1e-300)
+    return g, o
+
+
+# ---------------------------------------------------------------------------------------
+# BASELINE configs at full size (C1-C3), reduced sims for C4/C5 plus sampled full-size runs
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("lim", [W.LIM_UPWIND, W.LIM_VANLEER])
+def test_c1_growth_constant_G(lim):
+    _check(W.c1_growth(lim, M=1000))
+
+
+def test_c2_dissolution_full():
+    g, o = _check(W.c2_dissolution())
+    assert o["steps"][0] == 6000
+
+
+def test_c3_temperature_cycling_full():
+    g, o = _check(W.c3_cycling())
+    assert o["steps"][0] == 100_000
+
+
+@pytest.mark.parametrize("N", [1000, 4000])
+def test_c4_steps_mode(N):
+    _check(W.c4_sweep(N, batch=3, n_steps=200))
+
+
+def test_c5_tangents_small():
+    w = W.c5_ensemble(n_sims=18, N=300, t_max=60.0, M=60)
+    g, o = _check(w, mode=oracle.MODE_DUAL)
+    lo, go = oracle.loss_and_grad(o["samples"], o["tsamples"], w.target)
+    assert np.allclose(g["loss"], lo, rtol=1e-9, atol=0)
+    assert np.allclose(g["grad"], go, rtol=1e-8, atol=1e-9 * np.max(np.abs(go)))
+
+
+def test_c5_full_size_sampled_sims():
+    """C5 exactly as bench.py runs it (4096 sims x 2000 bins, 8 tangents) — oracle on 2 sims."""
+    w = W.c5_ensemble()
+    g = _gpu(w, want_n=False)
+    assert np.all(g["status"] == 0)
+    sims = [0, 4095]
+    o = oracle.run(w.subset(sims), mode=oracle.MODE_DUAL, threads=2, want_n=False)
+    gs = {k: g[k][sims] for k in ("samples", "tsamples", "status", "steps")}
+    assert np.array_equal(gs["steps"], o["steps"])
+    _cmp_samples(gs, o)
+    _cmp_tangents(gs, o)
+
+
+# ---------------------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("N", [3, 5, 31, 33, 257, 1023, 2049])
+def test_ragged_sizes(N):
+    w = W.c3_cycling(N=N, t_max=5.0, M=5, dt_max=0.05)
+    w.n0 = np.abs(np.random.default_rng(N).standard_normal((1, N))) * 100.0
+    _check(w)
+
+
+@pytest.mark.parametrize("P", [1, 3, 8, 10])
+def test_tangent_lane_counts(P):
+    w = W.c5_ensemble(n_sims=4, N=150, t_max=20.0, M=20, n_tangents=P)
+    _check(w, mode=oracle.MODE_DUAL)
+
+
+def test_custom_tangent_seed_over_solubility():
+    w = W.c5_ensemble(n_sims=2, N=120, t_max=10.0, M=10, n_tangents=2)
+    seed = np.zeros((2, 8 + 2))
+    seed[0, 8] = 1.0          # d/da (solubility prefactor)
+    seed[1, 0] = 0.5; seed[1, 9] = -2.0
+    w.tangent_seed = seed
+    _check(w, mode=oracle.MODE_DUAL)
+
+
+def test_dissolution_outflow_at_L0():
+    # strong dissolution drives mass through the L = 0 face (R-25)
+    w = W.c2_dissolution(N=400, t_max=200.0, M=50, dt_max=0.2)
+    w.n0 = W.gaussian_seed(400, 3.0, mean=40.0, sigma=10.0, m0=0.5)[None, :]
+    w.c0 = np.array([3.0])
+    g, o = _check(w)
+    assert o["samples"][0, -1, 2] < o["samples"][0, 0, 2]      # number left the domain
+
+
+def test_per_sim_n0_and_host_n0():
+    w = W.c4_sweep(2000, batch=4, n_steps=50)
+    rng = np.random.default_rng(0)
+    w.n0 = w.n0 * rng.uniform(0.5, 1.5, size=(4, 1))
+    _check(w)
+    _check(w, host_n0=True)
+
+
+def test_status_codes():
+    w = W.c1_growth(); w.dt_fixed = 30.0
+    _check(w)                                     # CFL error before the first step
+    w = W.c1_growth(); w.c0 = np.array([0.01])
+    _check(w)                                     # infeasible (c < 0)
+    w = W.c1_growth(); w.max_steps = 10
+    _check(w)                                     # max steps
+
+
+def test_determinism_independent_of_batch():
+    w = W.c5_ensemble(n_sims=40, N=200, t_max=20.0, M=20)
+    g_all = _gpu(w)
+    g_one = _gpu(w.subset([17]))
+    assert np.array_equal(g_all["samples"][17], g_one["samples"][0])
+    assert np.array_equal(g_all["tsamples"][17], g_one["tsamples"][0])
+    assert np.array_equal(g_all["n_final"][17], g_one["n_final"][0])
+    g_again = _gpu(w)
+    assert np.array_equal(g_all["samples"], g_again["samples"])
+
+
+def test_uncapped_cfl_tangents_vanish():
+    w = W.c4_sweep(500, batch=2, n_steps=50)
+    w.n_tangents = 6
+    g = _gpu(w)
+    assert np.all(g["ndot_final"] == 0.0)

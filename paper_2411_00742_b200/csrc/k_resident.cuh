@@ -33,8 +33,9 @@
 
 namespace pbe {
 
-// Smem halo: s_halo[(side * V + v) * NT + t], side 0/1 = bins 0/1 of thread t,
-// side 2/3 = bins K-2/K-1 (transposed so a warp's accesses are consecutive).
+// Smem halo: s_halo[(side * V + v) * HS + t + 1], HS = NT + 2, side 0/1 = bins 0/1 of
+// thread t, side 2/3 = bins K-2/K-1 (transposed so a warp's accesses are consecutive).
+// Columns 0 and NT + 1 stay zero: the ghost cells n_{-2} = n_{-1} = n_N = n_{N+1} = 0.
 template <int P, int K, bool NEG>
 __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* __restrict__ s_halo,
                                            int NT, int tid, double C, double kap, double beta,
@@ -42,15 +43,15 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
                                            double clip_thr) {
     constexpr int V = 1 + P;
     bool bad = false;
-    const bool has_l = tid > 0, has_r = tid + 1 < NT;
+    const int HS = NT + 2;
     // value of variable v at local bin j in [-2, K+1] (OLD values: the sweep order
     // guarantees x[v][j] is not yet updated when it is read here)
     auto X = [&](int v, int j) -> double {
         if (j >= 0 && j < K) return x[v][j];
-        if (j == -1) return has_l ? s_halo[(3 * V + v) * NT + tid - 1] : 0.0;
-        if (j == -2) return has_l ? s_halo[(2 * V + v) * NT + tid - 1] : 0.0;
-        if (j == K) return has_r ? s_halo[(0 * V + v) * NT + tid + 1] : 0.0;
-        return has_r ? s_halo[(1 * V + v) * NT + tid + 1] : 0.0;   // j == K + 1
+        if (j == -1) return s_halo[(3 * V + v) * HS + tid];
+        if (j == -2) return s_halo[(2 * V + v) * HS + tid];
+        if (j == K) return s_halo[(0 * V + v) * HS + tid + 2];
+        return s_halo[(1 * V + v) * HS + tid + 2];                 // j == K + 1
     };
     // flux through the face between local bins (f-1, f); returns primal F and fills Fd
     auto face = [&](int f, double (&Fd)[V]) -> double {
@@ -115,7 +116,7 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 
 // Grid: one CTA per simulation.  Block: NT = 32 NW threads with NT K >= N.
 // P = instantiated tangent lanes (>= kp.P; extra lanes carry zero seeds and stay 0).
-// Dynamic smem: 4 V NT doubles of halo.
+// Dynamic smem: 4 V (NT + 2) doubles of halo.
 template <int P, int K, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     constexpr int V = 1 + P;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     const int i0 = tid * K;
     const bool steps_mode = kp.n_steps > 0;
 
-    extern __shared__ double s_halo[];          // [4][V][NT]
+    extern __shared__ double s_halo[];          // [4][V][NT + 2]
     __shared__ double s_red[32][4][V];          // warp partial sums [warp][moment][value]
     __shared__ double s_C, s_kap, s_beta, s_Cd[PP], s_nscale;
     __shared__ int s_go, s_sample, s_bad;
@@ -157,15 +158,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         s_nscale = m;
     }
 
+    const int HS = NT + 2;
     auto publish_halo = [&]() {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            s_halo[(0 * V + v) * NT + tid] = x[v][0];
-            s_halo[(1 * V + v) * NT + tid] = x[v][1];
-            s_halo[(2 * V + v) * NT + tid] = x[v][K - 2];
-            s_halo[(3 * V + v) * NT + tid] = x[v][K - 1];
+            s_halo[(0 * V + v) * HS + tid + 1] = x[v][0];
+            s_halo[(1 * V + v) * HS + tid + 1] = x[v][1];
+            s_halo[(2 * V + v) * HS + tid + 1] = x[v][K - 2];
+            s_halo[(3 * V + v) * HS + tid + 1] = x[v][K - 1];
         }
     };
+    for (int j = tid; j < 4 * V; j += NT) { s_halo[j * HS] = 0.0; s_halo[j * HS + NT + 1] = 0.0; }
     // moment k partials of all V variables, warp-reduced into s_red[warp][k][*]
     auto moment_partials = [&](int kmom, int nv) {
         double acc[V];

@@ -91,7 +91,7 @@ struct ResidentVariant {
     int P, K, maxt;
     KernelFn fn;
 };
-size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)4 * (1 + v.P) * nt * sizeof(double); }
+size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)4 * (1 + v.P) * (nt + 2) * sizeof(double); }
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {
@@ -383,6 +383,10 @@ pbe_status pbe_tangents(pbe_ctx ctx, double* tangents, double* grad, int32_t on_
 pbe_status pbe_last_run_info(pbe_ctx ctx, pbe_run_info* info) {
     if (!ctx || !info) return fail(ctx, PBE_ERR_ARG, "NULL argument");
     if (!ctx->have_run) return fail(ctx, PBE_ERR_STATE, "no run yet");
+    if (ctx->info.main_ms < 0.0 && cudaEventQuery(ctx->ev1) == cudaSuccess) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) ctx->info.main_ms = ms;
+    }
     *info = ctx->info;
     return PBE_OK;
 }

@@ -183,19 +183,34 @@ __device__ __forceinline__ StepScalars time_step(const KParams& kp, D1 G, D1 t, 
 // Row a3: limited slope psi(a, b) = phi_vanLeer(a/b) * b = 2ab/(a+b) (ab > 0), else 0,
 // plus the partials pa = d psi/da = 2 (b/(a+b))^2 and pb = 2 (a/(a+b))^2 for tangents.
 // ------------------------------------------------------------------------------------
+// 1/x to ~1 ulp without the IEEE-division slow path (no branches): MUFU.RCP64H seed +
+// two Newton steps.  Callers guarantee 1e-300 < |x| < 1e300.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+// theta > 0  <=>  a and b non-zero with the same sign (no a*b underflow).  |a+b| <= 1e-300
+// (psi <= 2e-300) is treated as 0.
+__device__ __forceinline__ bool psi_active(double a, double b) {
+    return ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) && fabs(a + b) > 1e-300;
+}
 __device__ __forceinline__ double psi_vl(double a, double b) {
-    return (a * b > 0.0) ? (2.0 * a * b) / (a + b) : 0.0;
+    const bool on = psi_active(a, b);
+    const double r = rcp_nr(on ? a + b : 1.0);
+    return on ? 2.0 * a * (b * r) : 0.0;
 }
 __device__ __forceinline__ void psi_vl_d(double a, double b, double& psi, double& pa, double& pb) {
-    if (a * b > 0.0) {
-        const double r = 1.0 / (a + b);
-        const double br = b * r, ar = a * r;
-        psi = 2.0 * a * br;
-        pa = 2.0 * br * br;
-        pb = 2.0 * ar * ar;
-    } else {
-        psi = 0.0; pa = 0.0; pb = 0.0;
-    }
+    const bool on = psi_active(a, b);
+    const double r = rcp_nr(on ? a + b : 1.0);
+    const double br = b * r, ar = a * r;
+    psi = on ? 2.0 * a * br : 0.0;
+    pa = on ? 2.0 * br * br : 0.0;
+    pb = on ? 2.0 * ar * ar : 0.0;
 }
 
 // ------------------------------------------------------------------------------------

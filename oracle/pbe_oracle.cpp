@@ -376,7 +376,8 @@ template <> void seed_inputs<Dual>(const oracle_problem& pb, const double* th_s,
     for (int j = 0; j < Q; ++j) sol[j] = Dual(pb.sol[j]);
     for (int p = 0; p < pb.n_tan; ++p) {
         for (int j = 0; j < P + Q; ++j) {
-            const double s = pb.tangent_seed ? pb.tangent_seed[p * (P + Q) + j] : (j == p ? 1.0 : 0.0);
+            // NULL seed: unit vectors e_p over theta only (include/pbe.h); lanes p >= n_params are 0
+            const double s = pb.tangent_seed ? pb.tangent_seed[p * (P + Q) + j] : (j == p && j < P ? 1.0 : 0.0);
             if (j < P) th[j].d[p] = s; else sol[j - P].d[p] = s;
         }
     }
@@ -392,7 +393,7 @@ template <> void seed_inputs<cplx>(const oracle_problem& pb, const double* th_s,
     const int P = pb.n_params, Q = pb.n_sol;
     th.assign(P, cplx(0)); sol.assign(Q, cplx(0));
     for (int j = 0; j < P + Q; ++j) {
-        const double s = pb.tangent_seed ? pb.tangent_seed[lane * (P + Q) + j] : (j == lane ? 1.0 : 0.0);
+        const double s = pb.tangent_seed ? pb.tangent_seed[lane * (P + Q) + j] : (j == lane && j < P ? 1.0 : 0.0);
         if (j < P) th[j] = cplx(th_s[j], h * s); else sol[j - P] = cplx(pb.sol[j - P], h * s);
     }
 }

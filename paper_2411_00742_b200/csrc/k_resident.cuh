@@ -53,70 +53,86 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
         if (j == K) return s_halo[(0 * V + v) * HS + tid + 2];
         return s_halo[(1 * V + v) * HS + tid + 2];                 // j == K + 1
     };
-    // flux through the face between local bins (f-1, f); returns primal F and fills Fd
-    auto face = [&](int f, double (&Fd)[V]) -> double {
-        // C >= 0: a = d_{f-1}, b = d_f, upwind f-1.   C < 0: a = d_{f+1}, b = d_f, upwind f.
+    // Face between local bins (f-1, f).  For C >= 0: a = d_{f-1}, b = d_f, upwind f-1;
+    // for C < 0: a = d_{f+1}, b = d_f, upwind f.  Primal parts first (shared by all lanes).
+    double Fc = 0.0, Fdc[P > 0 ? P : 1];        // fluxes of the face shared with the previous bin
+    struct FaceP { double F, g, pak, pbk; };
+    auto face_primal = [&](int f) -> FaceP {
         const int u = NEG ? f : f - 1;
         const int ja = NEG ? f + 1 : f - 1;
         const double a = X(0, ja) - X(0, ja - 1), b = X(0, f) - X(0, f - 1);
         double ps = 0.0, pa = 0.0, pb = 0.0;
         if (vl) psi_vl_d(a, b, ps, pa, pb);
         const double nup = X(0, u);
-        const double F = fma(C, nup, kap * ps);
-        if (P > 0) {
-            const double g = fma(beta, ps, nup);
-            const double pak = kap * pa, pbk = kap * pb;
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const double ad = X(1 + p, ja) - X(1 + p, ja - 1), bd = X(1 + p, f) - X(1 + p, f - 1);
-                Fd[1 + p] = fma(Cd[p], g, fma(C, X(1 + p, u), fma(pak, ad, pbk * bd)));
-            }
-        }
-        return F;
+        FaceP r;
+        r.F = fma(C, nup, kap * ps);
+        r.g = fma(beta, ps, nup);
+        r.pak = kap * pa;
+        r.pbk = kap * pb;
+        return r;
     };
-    auto update = [&](int k, double Fl, double Fr, const double (&Fdl)[V], const double (&Fdr)[V]) {
+    auto face_lane = [&](int f, int p, const FaceP& fp) -> double {
+        const int u = NEG ? f : f - 1;
+        const int ja = NEG ? f + 1 : f - 1;
+        const double ad = X(1 + p, ja) - X(1 + p, ja - 1), bd = X(1 + p, f) - X(1 + p, f - 1);
+        return fma(Cd[p], fp.g, fma(C, X(1 + p, u), fma(fp.pak, ad, fp.pbk * bd)));
+    };
+    // update bin k from its two faces; the lane fluxes of the far face come from Fdc and
+    // are replaced in place by the near face's (so only one array of lane fluxes is live)
+    auto step_bin = [&](int k, int f_new, bool new_is_left) {
+        const FaceP fp = face_primal(f_new);
         const int i = i0 + k;
-        const double nn = x[0][k] - (Fr - Fl);
-        bool zero = (i >= N);
-        if (nn < 0.0) { if (nn >= -clip_thr) zero = true; else if (i < N) bad = true; }
-        x[0][k] = zero ? 0.0 : nn;
+        const double dF = new_is_left ? (Fc - fp.F) : (fp.F - Fc);
+        const double nn = x[0][k] - dF;
+        // clip (R-17): round-off negatives and ghost bins i >= N become exactly 0 (with their
+        // tangents); a real negative flags PBE_ERR_NEGATIVE.  Rare: warp-uniform slow path.
+        const bool zero = (i >= N) || (nn < 0.0 && nn >= -clip_thr);
+        bad |= (nn < -clip_thr) && (i < N);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const double nd = x[1 + p][k] - (Fdr[1 + p] - Fdl[1 + p]);
-            x[1 + p][k] = zero ? 0.0 : nd;
+            const double fl = face_lane(f_new, p, fp);     // reads OLD x[1+p][*] only
+            const double dFd = new_is_left ? (Fdc[p] - fl) : (fl - Fdc[p]);
+            Fdc[p] = fl;
+            x[1 + p][k] = x[1 + p][k] - dFd;
+        }
+        x[0][k] = zero ? 0.0 : nn;
+        Fc = fp.F;
+        if (P > 0 && __any_sync(0xffffffffu, zero)) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) x[1 + p][k] = zero ? 0.0 : x[1 + p][k];
         }
     };
 
-    double Fc, Fdc[V];
     if (!NEG) {
-        Fc = face(K, Fdc);                       // right face of bin K-1
+        {   // right face of bin K-1
+            const FaceP fp = face_primal(K);
+            Fc = fp.F;
 #pragma unroll
-        for (int k = K - 1; k >= 0; --k) {
-            double Fdl[V];
-            const double Fl = face(k, Fdl);      // left face of bin k (reads bins < k: old)
-            update(k, Fl, Fc, Fdl, Fdc);
-            Fc = Fl;
-#pragma unroll
-            for (int p = 0; p < P; ++p) Fdc[1 + p] = Fdl[1 + p];
+            for (int p = 0; p < P; ++p) Fdc[p] = face_lane(K, p, fp);
         }
+#pragma unroll
+        for (int k = K - 1; k >= 0; --k) step_bin(k, k, true);        // left face of bin k: reads bins < k (old)
     } else {
-        Fc = face(0, Fdc);                       // left face of bin 0
+        {   // left face of bin 0
+            const FaceP fp = face_primal(0);
+            Fc = fp.F;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double Fdr[V];
-            const double Fr = face(k + 1, Fdr);  // right face of bin k (reads bins > k: old)
-            update(k, Fc, Fr, Fdc, Fdr);
-            Fc = Fr;
-#pragma unroll
-            for (int p = 0; p < P; ++p) Fdc[1 + p] = Fdr[1 + p];
+            for (int p = 0; p < P; ++p) Fdc[p] = face_lane(0, p, fp);
         }
+#pragma unroll
+        for (int k = 0; k < K; ++k) step_bin(k, k + 1, false);        // right face of bin k: reads bins > k (old)
     }
     return bad;
 }
 
 // Grid: one CTA per simulation.  Block: NT = 32 NW threads with NT K >= N.
 // P = instantiated tangent lanes (>= kp.P; extra lanes carry zero seeds and stay 0).
-// Dynamic smem: 4 V (NT + 2) doubles of halo.
+// Dynamic smem: 2 parities x 4 V (NT + 2) doubles of halo.
+//
+// ONE CTA barrier per step: every warp keeps its own copy of the scalar state (c, t, mu3,
+// sample index, status) and evaluates the kinetics redundantly from the same smem partial
+// sums in the same order, so all warps take bitwise-identical decisions.  Halos, partial
+// sums and the negative-density flag are double-buffered by step parity.
 template <int P, int K, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     constexpr int V = 1 + P;
@@ -127,12 +143,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     const int NT = blockDim.x, NW = NT >> 5;
     const int N = kp.N;
     const int i0 = tid * K;
+    const int HS = NT + 2;
+    const int HP = 4 * V * HS;                  // doubles per halo parity
     const bool steps_mode = kp.n_steps > 0;
 
-    extern __shared__ double s_halo[];          // [4][V][NT + 2]
-    __shared__ double s_red[32][4][V];          // warp partial sums [warp][moment][value]
-    __shared__ double s_C, s_kap, s_beta, s_Cd[PP], s_nscale;
-    __shared__ int s_go, s_sample, s_bad;
+    extern __shared__ double s_halo[];          // [2][4][V][NT + 2], then LaneScal[NT]
+    __shared__ double s_red[2][32][4][V];       // [parity][warp][moment][value]
+    __shared__ long long s_bad[2];              // step index that produced a negative
+    __shared__ double s_nscale;
 
     double x[V][K];
     // ---- load n0 (tangents start at 0: n0 does not depend on theta, R-20) --------------
@@ -148,29 +166,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-    if (lane == 0) s_red[warp][0][0] = lmax;
-    if (tid == 0) s_bad = 0;
-    if (tid < PP) s_Cd[tid] = 0.0;               // lanes >= kp.P stay exactly 0
+    if (lane == 0) s_red[0][warp][0][0] = lmax;
+    if (tid < 2) s_bad[tid] = -1;
+    for (int j = tid; j < 8 * V; j += NT) { s_halo[j * HS] = 0.0; s_halo[j * HS + NT + 1] = 0.0; }
     __syncthreads();
     if (tid == 0) {
         double m = 0.0;
-        for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w][0][0]);
+        for (int w = 0; w < NW; ++w) m = fmax(m, s_red[0][w][0][0]);
         s_nscale = m;
     }
 
-    const int HS = NT + 2;
-    auto publish_halo = [&]() {
+    auto publish_halo = [&](int q) {
+        double* h = s_halo + q * HP;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            s_halo[(0 * V + v) * HS + tid + 1] = x[v][0];
-            s_halo[(1 * V + v) * HS + tid + 1] = x[v][1];
-            s_halo[(2 * V + v) * HS + tid + 1] = x[v][K - 2];
-            s_halo[(3 * V + v) * HS + tid + 1] = x[v][K - 1];
+            h[(0 * V + v) * HS + tid + 1] = x[v][0];
+            h[(1 * V + v) * HS + tid + 1] = x[v][1];
+            h[(2 * V + v) * HS + tid + 1] = x[v][K - 2];
+            h[(3 * V + v) * HS + tid + 1] = x[v][K - 1];
         }
     };
-    for (int j = tid; j < 4 * V; j += NT) { s_halo[j * HS] = 0.0; s_halo[j * HS + NT + 1] = 0.0; }
-    // moment k partials of all V variables, warp-reduced into s_red[warp][k][*]
-    auto moment_partials = [&](int kmom, int nv) {
+    // moment k partials of the first nv variables, warp-reduced into s_red[q][warp][k][*]
+    auto moment_partials = [&](int q, int kmom, int nv) {
         double acc[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = 0.0;
@@ -185,52 +202,60 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         }
         warp_transpose_reduce<V>(acc, lane);
         const int idx = reduce_index<V>(lane);
-        if (idx < V) s_red[warp][kmom][idx] = acc[0];
+        if (idx < V) s_red[q][warp][kmom][idx] = acc[0];
     };
 
     __syncthreads();
     const double clip_thr = 1e-12 * s_nscale;
-    moment_partials(3, 1);                       // mu3(n0)
-    publish_halo();
+    moment_partials(1, 3, 1);                   // mu3(n0): "step -1" outputs live in parity 1
+    publish_halo(1);
+    __syncthreads();
 
-    // ---- warp-0 scalar state (each lane: primal + its own tangent lane) ----------------
+    // ---- per-warp scalar state (lane p: primal + tangent p) ------------------------------
+    // Kept in smem between scalar phases (one slot per thread) so that the sweep has the
+    // register file to itself; only C, kap, beta and the lane tangents Cdot live across it.
+    struct LaneScal {
+        D1 c, t, mu3p, dt;
+        double loss, gacc, rms_c, rms_L;
+        long long nstep;
+        int m, status, landing;
+    };
+    LaneScal* s_ls = reinterpret_cast<LaneScal*>(s_halo + 2 * HP);
     const int pl = lane < kp.P ? lane : -1;
     const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl, kp.n_params,
                        kp.n_params + kp.n_sol};
     const double* kT = kp.knot_T + (size_t)s * kp.knotT_stride;
-    D1 c = mk(kp.c0[s]), t = mk(0.0), mu3p = mk(0.0), dt = mk(0.0);
-    bool landing = false;
-    int m = 0, status = ST_OK;
-    long long nstep = 0;
-    double loss = 0.0, gacc = 0.0, rms_c = 1.0, rms_L = 1.0;
     const bool has_target = kp.target != nullptr;
     const double* tgt = has_target ? kp.target + (size_t)s * kp.M * 2 : nullptr;
+    double C = 0.0, kap = 0.0, beta = 0.0, Cd_l = 0.0;
 
-    auto kinetics = [&]() -> bool {   // next step's C, kap (+ tangents); false on CFL error
-        const D1 T = temperature(kp, kT, t);
+    // kinetics + time step of the next step from scalar state L (row a1, a2)
+    auto kinetics = [&](LaneScal& L) -> bool {
+        const D1 T = temperature(kp, kT, L.t);
         const D1 cs = solubility(kp, KL, T);
-        const D1 S = c / cs;
+        const D1 S = L.c / cs;
         const D1 G = growth_rate(kp, KL, S, T);
-        const double tn = steps_mode ? 0.0 : kp.t_samples[m];
-        const StepScalars sc = time_step(kp, G, t, tn, steps_mode);
-        if (sc.err != ST_OK) { status = sc.err; return false; }
-        dt = sc.dt;
-        landing = sc.landing;
-        if (lane == 0) {
-            s_C = sc.C.v;
-            s_kap = sc.kap.v;
-            s_beta = sc.C.v > 0.0 ? 0.5 * (1.0 - 2.0 * sc.C.v) : (sc.C.v < 0.0 ? -0.5 * (1.0 + 2.0 * sc.C.v) : 0.0);
-        }
-        if (pl >= 0) s_Cd[pl] = sc.C.d;
+        const double tn = steps_mode ? 0.0 : kp.t_samples[L.m];
+        const StepScalars sc = time_step(kp, G, L.t, tn, steps_mode);
+        if (sc.err != ST_OK) { L.status = sc.err; return false; }
+        L.dt = sc.dt;
+        L.landing = sc.landing;
+        C = sc.C.v;
+        kap = sc.kap.v;
+        beta = C > 0.0 ? 0.5 * (1.0 - 2.0 * C) : (C < 0.0 ? -0.5 * (1.0 + 2.0 * C) : 0.0);  // kapdot = beta Cdot
+        Cd_l = sc.C.d;
         return true;
     };
 
-    __syncthreads();   // bar1 (prologue)
-    if (warp == 0) {
+    bool go = true, sample = false;
+    {
+        LaneScal L;
         double a = 0.0;
-        for (int w = 0; w < NW; ++w) a += s_red[w][3][0];
-        mu3p = mk(a, 0.0);
-        if (has_target) {
+        for (int w = 0; w < NW; ++w) a += s_red[1][w][3][0];
+        L.c = mk(kp.c0[s]); L.t = mk(0.0); L.mu3p = mk(a, 0.0); L.dt = mk(0.0);
+        L.loss = 0.0; L.gacc = 0.0; L.rms_c = 1.0; L.rms_L = 1.0;
+        L.nstep = 0; L.m = 0; L.status = ST_OK; L.landing = 0;
+        if (warp == 0 && has_target) {
             double sc2 = 0.0, sl2 = 0.0;
             for (int j = lane; j < kp.M; j += 32) { sc2 += tgt[2 * j] * tgt[2 * j]; sl2 += tgt[2 * j + 1] * tgt[2 * j + 1]; }
 #pragma unroll
@@ -238,90 +263,81 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
                 sc2 += __shfl_xor_sync(0xffffffffu, sc2, off);
                 sl2 += __shfl_xor_sync(0xffffffffu, sl2, off);
             }
-            rms_c = sqrt(sc2 / kp.M); rms_L = sqrt(sl2 / kp.M);
+            L.rms_c = sqrt(sc2 / kp.M); L.rms_L = sqrt(sl2 / kp.M);
         }
-        bool go = true;
-        if (kp.max_steps <= 0) { status = ST_MAXSTEPS; go = false; }
-        if (go) go = kinetics();
-        if (lane == 0) {
-            s_go = go;
-            s_sample = go && (landing || (steps_mode && kp.n_steps == 1));
-        }
+        if (kp.max_steps <= 0) { L.status = ST_MAXSTEPS; go = false; }
+        if (go) go = kinetics(L);
+        sample = go && (L.landing || (steps_mode && kp.n_steps == 1));
+        s_ls[tid] = L;
     }
-    __syncthreads();   // bar2 (prologue)
 
     const bool vl = kp.limiter == LIM_VANLEER;
-    while (s_go) {
-        const double C = s_C, kap = s_kap, beta = s_beta;
-        const bool sample = s_sample;
+    long long n = 0;
+    while (go) {
+        const int q = (int)(n & 1), qp = q ^ 1;
         double Cd[PP];
 #pragma unroll
-        for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? s_Cd[p] : 0.0;
+        for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? __shfl_sync(0xffffffffu, Cd_l, p) : 0.0;
 
         bool bad;
-        if (C >= 0.0) bad = sweep_bins<P, K, false>(x, s_halo, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
-        else          bad = sweep_bins<P, K, true>(x, s_halo, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
-        if (bad) s_bad = 1;
-        moment_partials(3, V);                   // mu3 of n and every tangent lane
+        const double* hin = s_halo + qp * HP;
+        if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+        else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+        if (bad) s_bad[q] = n;
+        moment_partials(q, 3, V);                // mu3 of n and every tangent lane
         if (sample) {
 #pragma unroll 1
-            for (int km = 0; km < 3; ++km) moment_partials(km, V);
+            for (int km = 0; km < 3; ++km) moment_partials(q, km, V);
         }
-        __syncthreads();   // bar1
-        publish_halo();
+        publish_halo(q);
+        __syncthreads();                         // the one barrier of the step
 
-        // ---- scalar phase (warp 0) -------------------------------------------------------
-        if (warp == 0) {
-            double tot[4] = {0.0, 0.0, 0.0, 0.0}, totd[4] = {0.0, 0.0, 0.0, 0.0};
+        // ---- scalar phase (every warp, identical arithmetic) -----------------------------
+        LaneScal L = s_ls[tid];
+        double tot[4] = {0.0, 0.0, 0.0, 0.0}, totd[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int km = 0; km < 4; ++km) {
-                if (km == 3 || sample) {
-                    double a = 0.0, b = 0.0;
-                    for (int w = 0; w < NW; ++w) {
-                        a += s_red[w][km][0];
-                        if (pl >= 0) b += s_red[w][km][1 + pl];
-                    }
-                    tot[km] = a; totd[km] = b;
+        for (int km = 0; km < 4; ++km) {
+            if (km == 3 || sample) {
+                double a = 0.0, b = 0.0;
+                for (int w = 0; w < NW; ++w) {
+                    a += s_red[q][w][km][0];
+                    if (pl >= 0) b += s_red[q][w][km][1 + pl];
                 }
-            }
-            const D1 mu3n = mk(tot[3], totd[3]);
-            const D1 cn = c - kp.rho_kv * (mu3n - mu3p);          // eq-discrete_mass_balance
-            bool go = true;
-            if (s_bad) { status = ST_NEG; go = false; }
-            else if (cn.v < 0.0) { status = ST_INFEAS; go = false; }
-            else {
-                c = cn; mu3p = mu3n;
-                t = landing ? mk(kp.t_samples[m], 0.0) : t + dt;
-                ++nstep;
-                if (sample) {
-                    const int mr = steps_mode ? 0 : m;
-                    double* r = kp.rec + ((size_t)s * kp.M + mr) * 6;
-                    if (lane == 0) { r[0] = t.v; r[1] = c.v; r[2] = tot[0]; r[3] = tot[1]; r[4] = tot[2]; r[5] = tot[3]; }
-                    if (pl >= 0) {
-                        double* rt = kp.trec + (((size_t)s * kp.M + mr) * kp.P + pl) * 5;
-                        rt[0] = c.d; rt[1] = totd[0]; rt[2] = totd[1]; rt[3] = totd[2]; rt[4] = totd[3];
-                    }
-                    if (has_target) {
-                        const double Lb = tot[1] / tot[0];
-                        const double Lbd = (totd[1] * tot[0] - tot[1] * totd[0]) / (tot[0] * tot[0]);
-                        const double rc = (c.v - tgt[2 * mr]) / rms_c, rL = (Lb - tgt[2 * mr + 1]) / rms_L;
-                        loss += rc * rc + rL * rL;
-                        gacc += 2.0 * (rc / rms_c) * c.d + 2.0 * (rL / rms_L) * Lbd;
-                    }
-                }
-                if (landing) ++m;
-                if (steps_mode ? (nstep >= kp.n_steps) : (m >= kp.M)) go = false;
-                else if (nstep >= kp.max_steps) { status = ST_MAXSTEPS; go = false; }
-                else go = kinetics();
-            }
-            __syncwarp();
-            if (lane == 0) {
-                s_bad = 0;
-                s_go = go;
-                s_sample = go && (landing || (steps_mode && nstep + 1 == kp.n_steps));
+                tot[km] = a; totd[km] = b;
             }
         }
-        __syncthreads();   // bar2
+        const D1 mu3n = mk(tot[3], totd[3]);
+        const D1 cn = L.c - kp.rho_kv * (mu3n - L.mu3p);        // eq-discrete_mass_balance
+        if (s_bad[q] == n) { L.status = ST_NEG; go = false; }
+        else if (cn.v < 0.0) { L.status = ST_INFEAS; go = false; }
+        else {
+            L.c = cn; L.mu3p = mu3n;
+            L.t = L.landing ? mk(kp.t_samples[L.m], 0.0) : L.t + L.dt;
+            ++L.nstep;
+            if (sample && warp == 0) {
+                const int mr = steps_mode ? 0 : L.m;
+                double* r = kp.rec + ((size_t)s * kp.M + mr) * 6;
+                if (lane == 0) { r[0] = L.t.v; r[1] = L.c.v; r[2] = tot[0]; r[3] = tot[1]; r[4] = tot[2]; r[5] = tot[3]; }
+                if (pl >= 0) {
+                    double* rt = kp.trec + (((size_t)s * kp.M + mr) * kp.P + pl) * 5;
+                    rt[0] = L.c.d; rt[1] = totd[0]; rt[2] = totd[1]; rt[3] = totd[2]; rt[4] = totd[3];
+                }
+                if (has_target) {
+                    const double Lb = tot[1] / tot[0];
+                    const double Lbd = (totd[1] * tot[0] - tot[1] * totd[0]) / (tot[0] * tot[0]);
+                    const double rc = (L.c.v - tgt[2 * mr]) / L.rms_c, rL = (Lb - tgt[2 * mr + 1]) / L.rms_L;
+                    L.loss += rc * rc + rL * rL;
+                    L.gacc += 2.0 * (rc / L.rms_c) * L.c.d + 2.0 * (rL / L.rms_L) * Lbd;
+                }
+            }
+            if (L.landing) ++L.m;
+            if (steps_mode ? (L.nstep >= kp.n_steps) : (L.m >= kp.M)) go = false;
+            else if (L.nstep >= kp.max_steps) { L.status = ST_MAXSTEPS; go = false; }
+            else go = kinetics(L);
+        }
+        sample = go && (L.landing || (steps_mode && L.nstep + 1 == kp.n_steps));
+        s_ls[tid] = L;
+        ++n;
     }
 
     // ---- epilogue -----------------------------------------------------------------------
@@ -342,14 +358,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         }
     }
     if (warp == 0) {
-        const bool ok = (status == ST_OK);
+        const LaneScal L = s_ls[tid];
+        const bool ok = (L.status == ST_OK);
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
         if (lane == 0) {
-            kp.status[s] = status;
-            kp.steps[s] = nstep;
-            if (kp.loss) kp.loss[s] = (has_target && ok) ? loss : qnan;
+            kp.status[s] = L.status;
+            kp.steps[s] = L.nstep;
+            if (kp.loss) kp.loss[s] = (has_target && ok) ? L.loss : qnan;
         }
-        if (pl >= 0 && kp.grad) kp.grad[(size_t)s * kp.P + pl] = (has_target && ok) ? gacc : qnan;
+        if (pl >= 0 && kp.grad) kp.grad[(size_t)s * kp.P + pl] = (has_target && ok) ? L.gacc : qnan;
     }
 }
 

@@ -91,7 +91,8 @@ struct ResidentVariant {
     int P, K, maxt;
     KernelFn fn;
 };
-size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)4 * (1 + v.P) * (nt + 2) * sizeof(double); }
+// halo (2 parities) + per-thread scalar state (LaneScal: 128 bytes)
+size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double) + (size_t)nt * 128; }
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {

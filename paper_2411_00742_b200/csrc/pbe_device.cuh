@@ -200,17 +200,17 @@ __device__ __forceinline__ bool psi_active(double a, double b) {
     return ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) && fabs(a + b) > 1e-300;
 }
 __device__ __forceinline__ double psi_vl(double a, double b) {
-    const bool on = psi_active(a, b);
-    const double r = rcp_nr(on ? a + b : 1.0);
-    return on ? 2.0 * a * (b * r) : 0.0;
+    const double r = psi_active(a, b) ? rcp_nr(a + b) : 0.0;
+    return 2.0 * a * (b * r);
 }
+// psi and its partials; an inactive face gets r = 0, which zeroes all three
 __device__ __forceinline__ void psi_vl_d(double a, double b, double& psi, double& pa, double& pb) {
-    const bool on = psi_active(a, b);
-    const double r = rcp_nr(on ? a + b : 1.0);
+    // a + b = 0 or subnormal gives r = NaN/inf, which the select discards
+    const double r = psi_active(a, b) ? rcp_nr(a + b) : 0.0;
     const double br = b * r, ar = a * r;
-    psi = on ? 2.0 * a * br : 0.0;
-    pa = on ? 2.0 * br * br : 0.0;
-    pb = on ? 2.0 * ar * ar : 0.0;
+    psi = 2.0 * a * br;
+    pa = 2.0 * br * br;
+    pb = 2.0 * ar * ar;
 }
 
 // ------------------------------------------------------------------------------------

@@ -29,6 +29,8 @@
 //  so only Cdot is lane-specific (8 FP64 ops per bin and lane).
 // =====================================================================================
 #pragma once
+#include <type_traits>
+
 #include "pbe_device.cuh"
 
 namespace pbe {
@@ -44,6 +46,7 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
     constexpr int V = 1 + P;
     bool bad = false;
     const int HS = NT + 2;
+    const double kap2 = 2.0 * kap, beta2 = 2.0 * beta;
     // value of variable v at local bin j in [-2, K+1] (OLD values: the sweep order
     // guarantees x[v][j] is not yet updated when it is read here)
     auto X = [&](int v, int j) -> double {
@@ -61,14 +64,14 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
         const int u = NEG ? f : f - 1;
         const int ja = NEG ? f + 1 : f - 1;
         const double a = X(0, ja) - X(0, ja - 1), b = X(0, f) - X(0, f - 1);
-        double ps = 0.0, pa = 0.0, pb = 0.0;
-        if (vl) psi_vl_d(a, b, ps, pa, pb);
+        double h = 0.0, qa = 0.0, qb = 0.0;          // psi = 2h, d psi/da = 2qa, d psi/db = 2qb
+        if (vl) psi_half_d(a, b, h, qa, qb);
         const double nup = X(0, u);
         FaceP r;
-        r.F = fma(C, nup, kap * ps);
-        r.g = fma(beta, ps, nup);
-        r.pak = kap * pa;
-        r.pbk = kap * pb;
+        r.F = fma(C, nup, kap2 * h);                   // C n_up + kap psi
+        r.g = fma(beta2, h, nup);                      // n_up + beta psi
+        r.pak = kap2 * qa;                             // kap d psi/da
+        r.pbk = kap2 * qb;                             // kap d psi/db
         return r;
     };
     auto face_lane = [&](int f, int p, const FaceP& fp) -> double {
@@ -146,6 +149,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     const int HS = NT + 2;
     const int HP = 4 * V * HS;                  // doubles per halo parity
     const bool steps_mode = kp.n_steps > 0;
+    const double L_half = kp.L_lo + 0.5 * kp.dL;          // centre of bin 0
+    const int red_idx = reduce_index<V>(lane);
 
     extern __shared__ double s_halo[];          // [2][4][V][NT + 2], then LaneScal[NT]
     __shared__ double s_red[2][32][4][V];       // [parity][warp][moment][value]
@@ -186,28 +191,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
             h[(3 * V + v) * HS + tid + 1] = x[v][K - 1];
         }
     };
-    // moment k partials of the first nv variables, warp-reduced into s_red[q][warp][k][*]
-    auto moment_partials = [&](int q, int kmom, int nv) {
+    // moment KM partials of all V variables, warp-reduced into s_red[q][warp][KM][*]
+    auto moment_partials = [&](int q, auto kmc) {
+        constexpr int KM = decltype(kmc)::value;
         double acc[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = 0.0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const double Lc = kp.L_lo + ((double)(i0 + k) + 0.5) * kp.dL;
+            const double Lc = fma((double)(i0 + k), kp.dL, L_half);   // bin centre
             double w = kp.dL;
-            for (int e = 0; e < kmom; ++e) w *= Lc;
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-                if (v < nv) acc[v] = fma(w, x[v][k], acc[v]);
+            for (int e = 0; e < KM; ++e) w *= Lc;
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = fma(w, x[v][k], acc[v]);
         }
         warp_transpose_reduce<V>(acc, lane);
-        const int idx = reduce_index<V>(lane);
-        if (idx < V) s_red[q][warp][kmom][idx] = acc[0];
+        if (red_idx < V) s_red[q][warp][KM][red_idx] = acc[0];
     };
 
     __syncthreads();
     const double clip_thr = 1e-12 * s_nscale;
-    moment_partials(1, 3, 1);                   // mu3(n0): "step -1" outputs live in parity 1
+    moment_partials(1, std::integral_constant<int, 3>{});   // mu3(n0): "step -1" outputs in parity 1
     publish_halo(1);
     __syncthreads();
 
@@ -284,10 +289,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
         else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
         if (bad) s_bad[q] = n;
-        moment_partials(q, 3, V);                // mu3 of n and every tangent lane
+        moment_partials(q, std::integral_constant<int, 3>{});     // mu3 of n and every tangent lane
         if (sample) {
-#pragma unroll 1
-            for (int km = 0; km < 3; ++km) moment_partials(q, km, V);
+            moment_partials(q, std::integral_constant<int, 0>{});
+            moment_partials(q, std::integral_constant<int, 1>{});
+            moment_partials(q, std::integral_constant<int, 2>{});
         }
         publish_halo(q);
         __syncthreads();                         // the one barrier of the step

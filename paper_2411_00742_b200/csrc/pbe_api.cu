@@ -302,7 +302,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     if (P) CUDA_TRY(ctx, cudaMemsetAsync(ctx->trec.p, 0xff, (size_t)n_sims * M * P * 5 * sizeof(double), st));
 
     KParams kp{};
-    kp.N = N; kp.L_lo = cf.L_lo; kp.dL = cf.dL; kp.limiter = cf.limiter;
+    kp.N = N; kp.L_lo = cf.L_lo; kp.dL = cf.dL; kp.inv_dL = 1.0 / cf.dL; kp.limiter = cf.limiter;
     kp.courant = cf.courant; kp.dt_fixed = cf.dt_fixed; kp.dt_max = cf.dt_max;
     kp.max_steps = cf.max_steps; kp.n_steps = cf.n_steps; kp.rho_kv = cf.rho_c * cf.k_v;
     kp.law = ctx->law; kp.n_params = ctx->n_params; kp.sol_kind = ctx->sol_kind; kp.n_sol = ctx->n_sol;

@@ -30,7 +30,7 @@ enum { ST_OK = 0, ST_CFL = 2, ST_NEG = 3, ST_INFEAS = 4, ST_MAXSTEPS = 5 };
 struct KParams {
     // grid and scheme
     int N;
-    double L_lo, dL;
+    double L_lo, dL, inv_dL;
     int limiter;
     double courant, dt_fixed, dt_max;
     long long max_steps, n_steps;
@@ -60,8 +60,20 @@ struct KParams {
     double* ndot_final;     // [S][P][N] or nullptr
 };
 
+// 1/x to ~1 ulp without the IEEE-division slow path (no branches): MUFU.RCP64H seed +
+// two Newton steps.  Callers guarantee 1e-300 < |x| < 1e300.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 // ------------------------------------------------------------------------------------
-// D1: value + one tangent (this lane's direction)
+// D1: value + one tangent (this lane's direction).  Divisions use rcp_nr (<= ~1 ulp off the
+// correctly rounded quotient, no slow path); operands are c*, S-like ratios and |G| > 1e-300.
 // ------------------------------------------------------------------------------------
 struct D1 { double v, d; };
 __device__ __forceinline__ D1 mk(double v, double d = 0.0) { return D1{v, d}; }
@@ -69,15 +81,20 @@ __device__ __forceinline__ D1 operator+(D1 a, D1 b) { return {a.v + b.v, a.d + b
 __device__ __forceinline__ D1 operator-(D1 a, D1 b) { return {a.v - b.v, a.d - b.d}; }
 __device__ __forceinline__ D1 operator-(D1 a) { return {-a.v, -a.d}; }
 __device__ __forceinline__ D1 operator*(D1 a, D1 b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
-__device__ __forceinline__ D1 operator/(D1 a, D1 b) { const double q = a.v / b.v; return {q, (a.d - q * b.d) / b.v}; }
+__device__ __forceinline__ D1 operator/(D1 a, D1 b) {
+    const double r = rcp_nr(b.v), q = a.v * r;
+    return {q, (a.d - q * b.d) * r};
+}
 __device__ __forceinline__ D1 operator+(D1 a, double b) { return {a.v + b, a.d}; }
 __device__ __forceinline__ D1 operator-(D1 a, double b) { return {a.v - b, a.d}; }
 __device__ __forceinline__ D1 operator+(double a, D1 b) { return {a + b.v, b.d}; }
 __device__ __forceinline__ D1 operator-(double a, D1 b) { return {a - b.v, -b.d}; }
 __device__ __forceinline__ D1 operator*(D1 a, double b) { return {a.v * b, a.d * b}; }
 __device__ __forceinline__ D1 operator*(double a, D1 b) { return {a * b.v, a * b.d}; }
-__device__ __forceinline__ D1 operator/(D1 a, double b) { return {a.v / b, a.d / b}; }
-__device__ __forceinline__ D1 operator/(double a, D1 b) { const double q = a / b.v; return {q, -q * b.d / b.v}; }
+__device__ __forceinline__ D1 operator/(double a, D1 b) {
+    const double r = rcp_nr(b.v), q = a * r;
+    return {q, -q * b.d * r};
+}
 __device__ __forceinline__ D1 dexp(D1 a) { const double e = exp(a.v); return {e, e * a.d}; }
 __device__ __forceinline__ D1 dlog(D1 a) { return {log(a.v), a.d / a.v}; }
 // |x| with d|x| = sgn(x) dx, sgn(0) = 0 (R-20)
@@ -154,11 +171,11 @@ __device__ __forceinline__ StepScalars time_step(const KParams& kp, D1 G, D1 t, 
     D1 dt, C;
     if (kp.dt_fixed > 0.0) {
         dt = mk(kp.dt_fixed);
-        C = G * dt / kp.dL;
+        C = G * dt * kp.inv_dL;
         if (fabs(C.v) > 1.0) r.err = ST_CFL;
-    } else if (G.v != 0.0) {
+    } else if (fabs(G.v) > 1e-300) {                 // |G| <= 1e-300 moves nothing: treated as 0
         const D1 dt_cfl = (kp.courant * kp.dL) / dabs(G);
-        if (kp.dt_max < dt_cfl.v) { dt = mk(kp.dt_max); C = G * dt / kp.dL; }
+        if (kp.dt_max < dt_cfl.v) { dt = mk(kp.dt_max); C = G * dt * kp.inv_dL; }
         else { dt = dt_cfl; C = mk(G.v > 0.0 ? kp.courant : -kp.courant); }   // C = nu sgn G (R-9)
     } else {
         dt = mk(kp.dt_max);
@@ -167,7 +184,7 @@ __device__ __forceinline__ StepScalars time_step(const KParams& kp, D1 G, D1 t, 
     if (!steps_mode) {
         if (t.v + dt.v >= tn - 1e-9 * dt.v) {
             const D1 dtl = tn - t;
-            const D1 Cl = G * dtl / kp.dL;
+            const D1 Cl = G * dtl * kp.inv_dL;
             if (fabs(Cl.v) <= 1.0) { dt = dtl; C = Cl; r.landing = true; }
         }
     } else if (isinf(dt.v)) {
@@ -183,82 +200,81 @@ __device__ __forceinline__ StepScalars time_step(const KParams& kp, D1 G, D1 t, 
 // Row a3: limited slope psi(a, b) = phi_vanLeer(a/b) * b = 2ab/(a+b) (ab > 0), else 0,
 // plus the partials pa = d psi/da = 2 (b/(a+b))^2 and pb = 2 (a/(a+b))^2 for tangents.
 // ------------------------------------------------------------------------------------
-// 1/x to ~1 ulp without the IEEE-division slow path (no branches): MUFU.RCP64H seed +
-// two Newton steps.  Callers guarantee 1e-300 < |x| < 1e300.
-__device__ __forceinline__ double rcp_nr(double x) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
-}
-
-// theta > 0  <=>  a and b non-zero with the same sign (no a*b underflow).  |a+b| <= 1e-300
-// (psi <= 2e-300) is treated as 0.
-__device__ __forceinline__ bool psi_active(double a, double b) {
-    return ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) && fabs(a + b) > 1e-300;
-}
+// theta = a/b > 0  <=>  ab > 0.  (If ab underflows, |a|,|b| < 1.5e-154 and psi <= 3e-154 is
+// taken as 0; if ab > 0 then |a+b| >= sqrt(ab) > 1.4e-154, safe for rcp_nr.)
 __device__ __forceinline__ double psi_vl(double a, double b) {
-    const double r = psi_active(a, b) ? rcp_nr(a + b) : 0.0;
-    return 2.0 * a * (b * r);
+    const double ab = a * b;
+    const double r = ab > 0.0 ? rcp_nr(a + b) : 0.0;
+    return 2.0 * ab * r;
 }
-// psi and its partials; an inactive face gets r = 0, which zeroes all three
-__device__ __forceinline__ void psi_vl_d(double a, double b, double& psi, double& pa, double& pb) {
-    // a + b = 0 or subnormal gives r = NaN/inf, which the select discards
-    const double r = psi_active(a, b) ? rcp_nr(a + b) : 0.0;
+// Half-slope and partials for the tangent lanes:  h = ab/(a+b) = psi/2,
+// qa = (b/(a+b))^2 = (d psi/da)/2,  qb = (a/(a+b))^2 = (d psi/db)/2  (0 for ab <= 0).
+__device__ __forceinline__ void psi_half_d(double a, double b, double& h, double& qa, double& qb) {
+    const double ab = a * b;
+    const double r = ab > 0.0 ? rcp_nr(a + b) : 0.0;   // inactive face: r = 0 zeroes all three
     const double br = b * r, ar = a * r;
-    psi = 2.0 * a * br;
-    pa = 2.0 * br * br;
-    pb = 2.0 * ar * ar;
+    h = ab * r;
+    qa = br * br;
+    qb = ar * ar;
 }
 
 // ------------------------------------------------------------------------------------
 // Transpose-reduce V per-lane values across a warp in ~V + 5 FP64 shuffles (instead of
 // 5 V): each level halves the list a lane keeps.  On exit, lane l holds in v[0] the warp
-// total of value index reduce_index<V>(l) (values >= V are padding).
+// total of value index reduce_index<V>(l) (== V for padding lanes).  Fully compile-time
+// (template recursion), so the list stays in registers.
 // ------------------------------------------------------------------------------------
-template <int V> struct RLevels {
-    // list sizes per level: V, ceil(V/2), ...  (up to 5 levels, bits 4..0)
-    __host__ __device__ static constexpr int n(int lvl) { return lvl == 0 ? V : (n(lvl - 1) + 1) / 2; }
+template <int V, int N, int LVL>
+struct TransposeReduce {
+    static __device__ __forceinline__ void run(double (&v)[V], int lane) {
+        constexpr int off = 16 >> LVL;
+        constexpr int H = (N + 1) / 2;
+        const bool hi = (lane & off) != 0;
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            const double upper = (H + j < N) ? v[(H + j < N) ? H + j : 0] : 0.0;
+            const double send = hi ? v[j] : upper;
+            const double keep = hi ? upper : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+        TransposeReduce<V, H, LVL + 1>::run(v, lane);
+    }
+};
+template <int V, int LVL>
+struct TransposeReduce<V, 1, LVL> {
+    static __device__ __forceinline__ void run(double (&v)[V], int) {
+#pragma unroll
+        for (int l = LVL; l < 5; ++l) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16 >> l);
+    }
+};
+template <int V, int N>
+struct TransposeReduce<V, N, 5> {   // more than 32 values: not used (V <= 11)
+    static __device__ __forceinline__ void run(double (&)[V], int) {}
+};
+template <int V>
+struct TransposeReduce<V, 1, 5> {
+    static __device__ __forceinline__ void run(double (&)[V], int) {}
 };
 
 template <int V>
+__device__ __forceinline__ void warp_transpose_reduce(double (&v)[V], int lane) {
+    TransposeReduce<V, V, 0>::run(v, lane);
+}
+
+template <int V>
 __device__ __forceinline__ int reduce_index(int lane) {
-    // position in the original list; returns V (= padding) when the lane's final slot is
-    // a pad entry of a shorter upper half
-    int idx = 0, real = V;
+    // position in the original list; V (= padding) when the lane's final slot is a pad
+    // entry of a shorter upper half
+    int idx = 0, real = V, n = V;
 #pragma unroll
     for (int lvl = 0; lvl < 5; ++lvl) {
-        const int n = RLevels<V>::n(lvl);
         if (n <= 1) break;
         const int h = (n + 1) / 2;
         if (lane & (16 >> lvl)) { idx += h; real -= h; }
         else if (real > h) real = h;
+        n = h;
     }
     return real >= 1 ? idx : V;
-}
-
-template <int V>
-__device__ __forceinline__ void warp_transpose_reduce(double (&v)[V], int lane) {
-#pragma unroll
-    for (int lvl = 0; lvl < 5; ++lvl) {
-        const int off = 16 >> lvl;
-        const int n = RLevels<V>::n(lvl);
-        if (n > 1) {
-            const int h = (n + 1) / 2;
-            const bool hi = (lane & off) != 0;
-#pragma unroll
-            for (int j = 0; j < h; ++j) {
-                const double upper = (h + j < n) ? v[(h + j < V) ? h + j : 0] : 0.0;
-                const double send = hi ? v[j] : upper;
-                const double keep = hi ? upper : v[j];
-                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-            }
-        } else {
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-        }
-    }
 }
 
 }  // namespace pbe

@@ -129,7 +129,10 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 }
 
 // Grid: one CTA per simulation.  Block: NT = 32 NW threads with NT K >= N.
-// P = instantiated tangent lanes (>= kp.P; extra lanes carry zero seeds and stay 0).
+// P = tangent lanes per CTA.  The kp.P lanes of a simulation are split into kp.G lane
+// groups of P: CTA b runs simulation b / G, group g = b % G, i.e. lanes [g P, g P + P)
+// (lanes >= kp.P carry zero seeds and stay 0).  Every group recomputes the primal march
+// (bitwise identically), so groups never communicate; group 0 writes the primal records.
 // Dynamic smem: 2 parities x 4 V (NT + 2) doubles of halo.
 //
 // ONE CTA barrier per step: every warp keeps its own copy of the scalar state (c, t, mu3,
@@ -141,7 +144,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     constexpr int V = 1 + P;
     constexpr int PP = P > 0 ? P : 1;
     static_assert(K >= 2, "K >= 2");
-    const int s = blockIdx.x;
+    const int s = blockIdx.x / kp.G;
+    const int grp = blockIdx.x - s * kp.G;
+    const int lane0 = grp * P;                                 // first tangent lane of the group
+    const int nl = P > 0 ? max(0, min(P, kp.P - lane0)) : 0;   // lanes of this group in use
+    const bool primal_out = (grp == 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
     const int N = kp.N;
@@ -226,8 +233,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         int m, status, landing;
     };
     LaneScal* s_ls = reinterpret_cast<LaneScal*>(s_halo + 2 * HP);
-    const int pl = lane < kp.P ? lane : -1;
-    const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl, kp.n_params,
+    const int pl = lane < nl ? lane : -1;                      // this lane's tangent within the group
+    const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl >= 0 ? lane0 + pl : -1, kp.n_params,
                        kp.n_params + kp.n_sol};
     const double* kT = kp.knot_T + (size_t)s * kp.knotT_stride;
     const bool has_target = kp.target != nullptr;
@@ -323,9 +330,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
             if (sample && warp == 0) {
                 const int mr = steps_mode ? 0 : L.m;
                 double* r = kp.rec + ((size_t)s * kp.M + mr) * 6;
-                if (lane == 0) { r[0] = L.t.v; r[1] = L.c.v; r[2] = tot[0]; r[3] = tot[1]; r[4] = tot[2]; r[5] = tot[3]; }
+                if (lane == 0 && primal_out) { r[0] = L.t.v; r[1] = L.c.v; r[2] = tot[0]; r[3] = tot[1]; r[4] = tot[2]; r[5] = tot[3]; }
                 if (pl >= 0) {
-                    double* rt = kp.trec + (((size_t)s * kp.M + mr) * kp.P + pl) * 5;
+                    double* rt = kp.trec + (((size_t)s * kp.M + mr) * kp.P + lane0 + pl) * 5;
                     rt[0] = L.c.d; rt[1] = totd[0]; rt[2] = totd[1]; rt[3] = totd[2]; rt[4] = totd[3];
                 }
                 if (has_target) {
@@ -347,18 +354,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     }
 
     // ---- epilogue -----------------------------------------------------------------------
-    if (kp.n_final) {
+    if (kp.n_final && primal_out) {
 #pragma unroll
         for (int k = 0; k < K; ++k) { const int i = i0 + k; if (i < N) kp.n_final[(size_t)s * N + i] = x[0][k]; }
     }
     if (kp.ndot_final) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            if (p < kp.P) {
+            if (p < nl) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const int i = i0 + k;
-                    if (i < N) kp.ndot_final[((size_t)s * kp.P + p) * N + i] = x[1 + p][k];
+                    if (i < N) kp.ndot_final[((size_t)s * kp.P + lane0 + p) * N + i] = x[1 + p][k];
                 }
             }
         }
@@ -367,12 +374,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         const LaneScal L = s_ls[tid];
         const bool ok = (L.status == ST_OK);
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-        if (lane == 0) {
+        if (lane == 0 && primal_out) {
             kp.status[s] = L.status;
             kp.steps[s] = L.nstep;
             if (kp.loss) kp.loss[s] = (has_target && ok) ? L.loss : qnan;
         }
-        if (pl >= 0 && kp.grad) kp.grad[(size_t)s * kp.P + pl] = (has_target && ok) ? L.gacc : qnan;
+        if (pl >= 0 && kp.grad) kp.grad[(size_t)s * kp.P + lane0 + pl] = (has_target && ok) ? L.gacc : qnan;
     }
 }
 

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -60,6 +61,7 @@ struct pbe_ctx_s {
     cudaStream_t last_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     pbe_run_info info{};
+    int group_max = 4;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {
@@ -96,25 +98,29 @@ size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * 
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {
-    RV(0, 2, 512),  RV(0, 4, 512),  RV(0, 8, 512),  RV(0, 16, 512),
-    RV(2, 2, 512),  RV(2, 4, 512),  RV(2, 8, 512),  RV(2, 16, 256),
-    RV(4, 2, 512),  RV(4, 4, 512),  RV(4, 8, 256),
-    RV(8, 2, 256),  RV(8, 4, 256),  RV(8, 8, 256),
-    RV(10, 2, 256), RV(10, 4, 256),
+    RV(0, 2, 512), RV(0, 4, 512), RV(0, 8, 512), RV(0, 16, 512),
+    RV(2, 2, 512), RV(2, 4, 512), RV(2, 8, 512), RV(2, 16, 256),
+    RV(4, 2, 512), RV(4, 4, 512), RV(4, 8, 256),
+    RV(5, 2, 512), RV(5, 4, 512), RV(5, 8, 256),
+    RV(8, 2, 256), RV(8, 4, 256), RV(8, 8, 256),
 };
 #undef RV
 
-int lanes_instantiated(int P) {
+// Tangent lanes per CTA.  More than `group_max` lanes are split into lane groups (one CTA
+// each, primal recomputed): fewer registers per thread -> 16 warps per SM instead of 8.
+int lanes_per_cta(int P, int group_max) {
     if (P == 0) return 0;
     if (P <= 2) return 2;
     if (P <= 4) return 4;
-    if (P <= 8) return 8;
-    return 10;
+    if (group_max >= 8 && P <= 8) return 8;
+    if (P <= 8) return 4;          // 2 groups of 4
+    return 5;                      // 9..10 lanes: 2 groups of 5
 }
 
-// smallest K (fewest registers per thread) whose CTA covers N bins
-const ResidentVariant* pick_resident(int N, int P) {
-    const int Pi = lanes_instantiated(P);
+// smallest K (most warps) whose CTA covers N bins
+const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups) {
+    const int Pi = lanes_per_cta(P, group_max);
+    *groups = Pi ? (P + Pi - 1) / Pi : 1;
     const ResidentVariant* best = nullptr;
     for (const auto& v : kResident) {
         if (v.P != Pi) continue;
@@ -165,6 +171,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
 
     pbe_ctx ctx = new pbe_ctx_s();
     ctx->cfg = c;
+    if (const char* e = getenv("PBE_LANES_PER_CTA")) ctx->group_max = atoi(e);
     ctx->device = device;
     const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
     cudaError_t ea = cudaSuccess;
@@ -274,7 +281,8 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
 
     // kernel choice
-    const ResidentVariant* rv = pick_resident(N, P);
+    int groups = 1;
+    const ResidentVariant* rv = pick_resident(N, P, ctx->group_max, &groups);
     int kind = cf.kernel == PBE_KERNEL_AUTO ? PBE_KERNEL_RESIDENT : cf.kernel;
     if (kind != PBE_KERNEL_RESIDENT)
         return fail(ctx, PBE_ERR_ARG, "kernel variant %d not available in this build", kind);
@@ -309,7 +317,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     kp.n_knots = ctx->n_knots; kp.knotT_stride = ctx->knotT_per_sim ? ctx->n_knots : 0;
     kp.theta = ctx->theta.as<double>(); kp.sol = ctx->sol.as<double>(); kp.knot_t = ctx->knot_t.as<double>();
     kp.knot_T = ctx->knot_T.as<double>(); kp.seed = ctx->seed.as<double>();
-    kp.n_sims = n_sims; kp.M = M; kp.P = P;
+    kp.n_sims = n_sims; kp.M = M; kp.P = P; kp.G = groups;
     kp.n0 = n0_dev; kp.n0_stride = n0_stride; kp.c0 = ctx->c0.as<double>();
     kp.t_samples = ctx->tsamp.as<double>(); kp.target = target ? ctx->target.as<double>() : nullptr;
     kp.rec = ctx->rec.as<double>(); kp.trec = ctx->trec.as<double>(); kp.status = ctx->status.as<int>();
@@ -320,7 +328,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     const size_t smem = resident_smem(*rv, nt);
     CUDA_TRY(ctx, cudaFuncSetAttribute(rv->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    rv->fn<<<n_sims, nt, smem, st>>>(kp);
+    rv->fn<<<n_sims * groups, nt, smem, st>>>(kp);
     CUDA_TRY(ctx, cudaGetLastError());
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
 
@@ -328,7 +336,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     ctx->info.kernel = PBE_KERNEL_RESIDENT;
     ctx->info.launches = 1;
     ctx->info.threads_per_cta = nt;
-    ctx->info.ctas = n_sims;
+    ctx->info.ctas = n_sims * groups;
     ctx->info.cluster = 1;
     ctx->info.bins_per_thread = rv->K;
     ctx->info.main_ms = -1.0;

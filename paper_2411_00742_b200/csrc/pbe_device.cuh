@@ -44,7 +44,8 @@ struct KParams {
     const double* knot_T;   // [S or 1][n_knots]
     const double* seed;     // [P][n_params + n_sol]
     // batch
-    int n_sims, M, P;       // P = tangent lanes requested (<= instantiated lanes)
+    int n_sims, M, P;       // P = tangent lanes of a simulation
+    int G;                  // lane groups per simulation (CTAs per simulation)
     const double* n0; long long n0_stride;
     const double* c0;       // [S]
     const double* t_samples;// [M]

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     const double L_half = kp.L_lo + 0.5 * kp.dL;          // centre of bin 0
     const int red_idx = reduce_index<V>(lane);
 
-    extern __shared__ double s_halo[];          // [2][4][V][NT + 2], then LaneScal[NT]
+    extern __shared__ double s_halo[];          // [2][4][V][NT + 2], WarpPart[32], LanePart[NT]
     __shared__ double s_red[2][32][4][V];       // [parity][warp][moment][value]
     __shared__ long long s_bad[2];              // step index that produced a negative
     __shared__ double s_nscale;
@@ -232,7 +232,27 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         long long nstep;
         int m, status, landing;
     };
-    LaneScal* s_ls = reinterpret_cast<LaneScal*>(s_halo + 2 * HP);
+    // smem copy: primal part once per warp (identical in all lanes), tangent part per lane
+    struct WarpPart { double c, t, mu3p, dt, loss, rms_c, rms_L; long long nstep; int m, status, landing; };
+    struct LanePart { double c, t, mu3p, dt, gacc; };
+    WarpPart* s_wp = reinterpret_cast<WarpPart*>(s_halo + 2 * HP);
+    LanePart* s_lp = reinterpret_cast<LanePart*>(s_wp + 32);
+    auto load_ls = [&]() -> LaneScal {
+        const WarpPart w = s_wp[warp];
+        const LanePart l = s_lp[tid];
+        LaneScal L;
+        L.c = mk(w.c, l.c); L.t = mk(w.t, l.t); L.mu3p = mk(w.mu3p, l.mu3p); L.dt = mk(w.dt, l.dt);
+        L.loss = w.loss; L.gacc = l.gacc; L.rms_c = w.rms_c; L.rms_L = w.rms_L;
+        L.nstep = w.nstep; L.m = w.m; L.status = w.status; L.landing = w.landing;
+        return L;
+    };
+    auto store_ls = [&](const LaneScal& L) {
+        __syncwarp();
+        if (lane == 0)
+            s_wp[warp] = WarpPart{L.c.v, L.t.v, L.mu3p.v, L.dt.v, L.loss, L.rms_c, L.rms_L, L.nstep, L.m,
+                                  L.status, L.landing};
+        s_lp[tid] = LanePart{L.c.d, L.t.d, L.mu3p.d, L.dt.d, L.gacc};
+    };
     const int pl = lane < nl ? lane : -1;                      // this lane's tangent within the group
     const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl >= 0 ? lane0 + pl : -1, kp.n_params,
                        kp.n_params + kp.n_sol};
@@ -280,7 +300,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         if (kp.max_steps <= 0) { L.status = ST_MAXSTEPS; go = false; }
         if (go) go = kinetics(L);
         sample = go && (L.landing || (steps_mode && kp.n_steps == 1));
-        s_ls[tid] = L;
+        store_ls(L);
     }
 
     const bool vl = kp.limiter == LIM_VANLEER;
@@ -306,7 +326,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         __syncthreads();                         // the one barrier of the step
 
         // ---- scalar phase (every warp, identical arithmetic) -----------------------------
-        LaneScal L = s_ls[tid];
+        LaneScal L = load_ls();
         double tot[4] = {0.0, 0.0, 0.0, 0.0}, totd[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int km = 0; km < 4; ++km) {
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
             else go = kinetics(L);
         }
         sample = go && (L.landing || (steps_mode && L.nstep + 1 == kp.n_steps));
-        s_ls[tid] = L;
+        store_ls(L);
         ++n;
     }
 
@@ -371,7 +391,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         }
     }
     if (warp == 0) {
-        const LaneScal L = s_ls[tid];
+        __syncwarp();
+        const LaneScal L = load_ls();
         const bool ok = (L.status == ST_OK);
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
         if (lane == 0 && primal_out) {

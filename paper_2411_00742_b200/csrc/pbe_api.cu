@@ -93,8 +93,8 @@ struct ResidentVariant {
     int P, K, maxt;
     KernelFn fn;
 };
-// halo (2 parities) + per-thread scalar state (LaneScal: 128 bytes)
-size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double) + (size_t)nt * 128; }
+// halo (2 parities) + scalar state (WarpPart[32] <= 96 B, LanePart[nt] = 40 B)
+size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double) + 32 * 96 + (size_t)nt * 40; }
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {
@@ -125,6 +125,8 @@ const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups) {
     for (const auto& v : kResident) {
         if (v.P != Pi) continue;
         if ((long long)v.K * v.maxt < N) continue;
+        const int nt = ((N + v.K - 1) / v.K + 31) / 32 * 32;
+        if (resident_smem(v, nt) > 200 * 1024) continue;      // + <= 20 KB static < 227 KB
         if (!best || v.K < best->K) best = &v;
     }
     return best;

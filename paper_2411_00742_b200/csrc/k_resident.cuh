@@ -82,15 +82,12 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
     };
     // update bin k from its two faces; the lane fluxes of the far face come from Fdc and
     // are replaced in place by the near face's (so only one array of lane fluxes is live)
+    bool neg = false;
     auto step_bin = [&](int k, int f_new, bool new_is_left) {
         const FaceP fp = face_primal(f_new);
-        const int i = i0 + k;
         const double dF = new_is_left ? (Fc - fp.F) : (fp.F - Fc);
         const double nn = x[0][k] - dF;
-        // clip (R-17): round-off negatives and ghost bins i >= N become exactly 0 (with their
-        // tangents); a real negative flags PBE_ERR_NEGATIVE.  Rare: warp-uniform slow path.
-        const bool zero = (i >= N) || (nn < 0.0 && nn >= -clip_thr);
-        bad |= (nn < -clip_thr) && (i < N);
+        neg |= (nn < 0.0);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const double fl = face_lane(f_new, p, fp);     // reads OLD x[1+p][*] only
@@ -98,14 +95,9 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
             Fdc[p] = fl;
             x[1 + p][k] = x[1 + p][k] - dFd;
         }
-        x[0][k] = zero ? 0.0 : nn;
+        x[0][k] = nn;
         Fc = fp.F;
-        if (P > 0 && __any_sync(0xffffffffu, zero)) {
-#pragma unroll
-            for (int p = 0; p < P; ++p) x[1 + p][k] = zero ? 0.0 : x[1 + p][k];
-        }
     };
-
     if (!NEG) {
         {   // right face of bin K-1
             const FaceP fp = face_primal(K);
@@ -124,6 +116,22 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) step_bin(k, k + 1, false);        // right face of bin k: reads bins > k (old)
+    }
+    // Clip (R-17), applied after the sweep (every face above used OLD values, so deferring
+    // it is exact): round-off negatives and ghost bins i >= N become exactly 0 together with
+    // their tangents; a negative below -clip_thr flags PBE_ERR_NEGATIVE.  Warp-uniform slow
+    // path, taken only by warps holding padding bins or a negative.
+    if (__any_sync(0xffffffffu, neg || (i0 + K > N))) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = i0 + k;
+            const double nn = x[0][k];
+            const bool zero = (i >= N) || (nn < 0.0 && nn >= -clip_thr);
+            bad |= (nn < -clip_thr) && (i < N);
+            x[0][k] = zero ? 0.0 : nn;
+#pragma unroll
+            for (int p = 0; p < P; ++p) x[1 + p][k] = zero ? 0.0 : x[1 + p][k];
+        }
     }
     return bad;
 }

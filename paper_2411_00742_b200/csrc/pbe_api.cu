@@ -61,7 +61,7 @@ struct pbe_ctx_s {
     cudaStream_t last_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     pbe_run_info info{};
-    int group_max = 4;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
+    int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {

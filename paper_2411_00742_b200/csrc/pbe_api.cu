@@ -17,6 +17,7 @@
 #include "../../include/pbe.h"
 #include "pbe_device.cuh"
 #include "k_resident.cuh"
+#include "k_stream.cuh"
 
 using pbe::KParams;
 
@@ -55,6 +56,8 @@ struct pbe_ctx_s {
     DevBuf c0, tsamp, target, n0_staged;
     // outputs
     DevBuf rec, trec, status, steps, loss, grad;
+    // streaming-kernel scratch (allocated on first use)
+    DevBuf sbuf, spart, sbar, sfinal, snscale;
     // last run
     bool have_run = false;
     int last_sims = 0;
@@ -106,6 +109,22 @@ const ResidentVariant kResident[] = {
 };
 #undef RV
 
+// k_stream<P> variants: lanes per launch (the tangent lanes of a simulation are never split)
+struct StreamVariant {
+    int P;
+    const void* fn;
+    void (*load)(const double*, long long, int, int, double*, long long, unsigned long long*);
+    void (*store)(const double*, const double*, const int*, int, int, long long, double*, double*);
+};
+#define SV(P) StreamVariant{P, (const void*)&pbe::k_stream<P>, &pbe::k_stream_load<1 + P>, &pbe::k_stream_store<1 + P>}
+const StreamVariant kStream[] = {SV(0), SV(2), SV(4)};
+#undef SV
+const StreamVariant* pick_stream(int P) {
+    for (const auto& v : kStream)
+        if (v.P >= P) return &v;
+    return nullptr;
+}
+
 // Tangent lanes per CTA.  More than `group_max` lanes are split into lane groups (one CTA
 // each, primal recomputed): fewer registers per thread -> 16 warps per SM instead of 8.
 int lanes_per_cta(int P, int group_max) {
@@ -133,6 +152,76 @@ const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------------------------
+// k_stream launch: padded ping-pong state in ctx scratch, load kernel, one cooperative
+// launch for the whole march, store kernel for n_final / ndot_final.
+// ------------------------------------------------------------------------------------
+static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp, int S, const double* n0,
+                                long long n0_stride, cudaStream_t st) {
+    const int N = kp.N, V = 1 + sv.P;
+    const long long pitch = ((long long)N + 4 + 3) / 4 * 4;
+    int dev = ctx->device, sms = 0;
+    CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // occupancy of the cooperative kernel (smem depends on TB: pick TB first for 2 CTAs/SM)
+    const long long work = (long long)S * N;
+    int TB = 4096;
+    while (TB > 256 && work / TB < 4LL * 2 * sms) TB >>= 1;
+    const size_t smem = (size_t)2 * V * (TB + 4) * sizeof(double);
+    CUDA_TRY(ctx, cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sv.fn, pbe::STREAM_NT, smem));
+    if (per_sm < 1) return fail(ctx, PBE_ERR_CUDA, "k_stream does not fit on an SM (smem %zu)", smem);
+    per_sm = per_sm > 2 ? 2 : per_sm;
+    const int G = per_sm * sms;
+    const int T_sim = (N + TB - 1) / TB;
+    const long long n_tiles = (long long)S * T_sim;
+    const long long chunk = (n_tiles + G - 1) / G;
+    if ((chunk + T_sim - 1) / T_sim + 1 > pbe::STREAM_MAXS)
+        return fail(ctx, PBE_ERR_ARG, "too many simulations per CTA for the streaming kernel (S = %d, N = %d)", S, N);
+
+    const size_t buf_el = (size_t)S * V * pitch;
+    CUDA_TRY(ctx, ctx->sbuf.ensure(2 * buf_el * sizeof(double)));
+    CUDA_TRY(ctx, ctx->spart.ensure((size_t)S * T_sim * 5 * V * sizeof(double)));
+    CUDA_TRY(ctx, ctx->sbar.ensure(8 * sizeof(unsigned)));
+    CUDA_TRY(ctx, ctx->sfinal.ensure((size_t)S * sizeof(int)));
+    CUDA_TRY(ctx, ctx->snscale.ensure((size_t)S * sizeof(unsigned long long)));
+    double* b0 = ctx->sbuf.as<double>();
+    double* b1 = b0 + buf_el;
+    // ghosts and padding must be zero in both buffers (only interior bins are ever written)
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbuf.p, 0, 2 * buf_el * sizeof(double), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbar.p, 0, 8 * sizeof(unsigned), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->snscale.p, 0, (size_t)S * sizeof(unsigned long long), st));
+    const dim3 lg((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, S);
+    sv.load<<<lg, 256, 0, st>>>(n0, n0_stride, N, S, b0, pitch, ctx->snscale.as<unsigned long long>());
+    CUDA_TRY(ctx, cudaGetLastError());
+
+    pbe::StreamParams sp{};
+    sp.kp = kp;
+    sp.buf0 = b0; sp.buf1 = b1; sp.pitch = pitch; sp.TB = TB; sp.T_sim = T_sim; sp.n_tiles = n_tiles;
+    sp.part = ctx->spart.as<double>();
+    sp.bar = ctx->sbar.as<unsigned>();
+    sp.active = reinterpret_cast<int*>(ctx->sbar.as<unsigned>() + 4);
+    sp.final_buf = ctx->sfinal.as<int>();
+    sp.nscale_bits = ctx->snscale.as<unsigned long long>();
+    void* args[] = {&sp};
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel(sv.fn, dim3(G), dim3(pbe::STREAM_NT), args, smem, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+    int launches = 2;
+    if (kp.n_final || kp.ndot_final) {
+        sv.store<<<lg, 256, 0, st>>>(b0, b1, sp.final_buf, N, kp.P, pitch, kp.n_final, kp.ndot_final);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
+    ctx->info.kernel = PBE_KERNEL_STREAM;
+    ctx->info.launches = launches;
+    ctx->info.threads_per_cta = pbe::STREAM_NT;
+    ctx->info.ctas = G;
+    ctx->info.cluster = 1;
+    ctx->info.bins_per_thread = 0;
+    return PBE_OK;
+}
 
 // ------------------------------------------------------------------------------------
 // C ABI
@@ -202,7 +291,7 @@ void pbe_destroy(pbe_ctx ctx) {
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->theta, &ctx->sol, &ctx->knot_t, &ctx->knot_T, &ctx->seed, &ctx->c0, &ctx->tsamp,
                       &ctx->target, &ctx->n0_staged, &ctx->rec, &ctx->trec, &ctx->status, &ctx->steps,
-                      &ctx->loss, &ctx->grad})
+                      &ctx->loss, &ctx->grad, &ctx->sbuf, &ctx->spart, &ctx->sbar, &ctx->sfinal, &ctx->snscale})
         b->release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -282,13 +371,18 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     }
     if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
 
-    // kernel choice
+    // kernel choice: register-resident when the simulation fits one CTA, else streaming
     int groups = 1;
     const ResidentVariant* rv = pick_resident(N, P, ctx->group_max, &groups);
-    int kind = cf.kernel == PBE_KERNEL_AUTO ? PBE_KERNEL_RESIDENT : cf.kernel;
-    if (kind != PBE_KERNEL_RESIDENT)
+    const StreamVariant* sv = pick_stream(P);
+    int kind = cf.kernel;
+    if (kind == PBE_KERNEL_AUTO) kind = rv ? PBE_KERNEL_RESIDENT : PBE_KERNEL_STREAM;
+    if (kind == PBE_KERNEL_CLUSTER)
         return fail(ctx, PBE_ERR_ARG, "kernel variant %d not available in this build", kind);
-    if (!rv) return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit the resident kernel", N, P);
+    if (kind == PBE_KERNEL_RESIDENT && !rv)
+        return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit the resident kernel", N, P);
+    if (kind == PBE_KERNEL_STREAM && !sv)
+        return fail(ctx, PBE_ERR_ARG, "the streaming kernel supports at most 4 tangent lanes (got %d)", P);
 
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
@@ -326,21 +420,25 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     kp.steps = ctx->steps.as<long long>(); kp.loss = ctx->loss.as<double>(); kp.grad = ctx->grad.as<double>();
     kp.n_final = n_final; kp.ndot_final = ndot_final;
 
-    const int nt = ((N + rv->K - 1) / rv->K + 31) / 32 * 32;
-    const size_t smem = resident_smem(*rv, nt);
-    CUDA_TRY(ctx, cudaFuncSetAttribute(rv->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    rv->fn<<<n_sims * groups, nt, smem, st>>>(kp);
-    CUDA_TRY(ctx, cudaGetLastError());
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
-
     ctx->info = pbe_run_info{};
-    ctx->info.kernel = PBE_KERNEL_RESIDENT;
-    ctx->info.launches = 1;
-    ctx->info.threads_per_cta = nt;
-    ctx->info.ctas = n_sims * groups;
-    ctx->info.cluster = 1;
-    ctx->info.bins_per_thread = rv->K;
+    if (kind == PBE_KERNEL_RESIDENT) {
+        const int nt = ((N + rv->K - 1) / rv->K + 31) / 32 * 32;
+        const size_t smem = resident_smem(*rv, nt);
+        CUDA_TRY(ctx, cudaFuncSetAttribute(rv->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+        rv->fn<<<n_sims * groups, nt, smem, st>>>(kp);
+        CUDA_TRY(ctx, cudaGetLastError());
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+        ctx->info.kernel = PBE_KERNEL_RESIDENT;
+        ctx->info.launches = 1;
+        ctx->info.threads_per_cta = nt;
+        ctx->info.ctas = n_sims * groups;
+        ctx->info.cluster = 1;
+        ctx->info.bins_per_thread = rv->K;
+    } else {
+        pbe_status r = launch_stream(ctx, *sv, kp, n_sims, n0_dev, n0_stride, st);
+        if (r != PBE_OK) return r;
+    }
     ctx->info.main_ms = -1.0;
     ctx->have_run = true;
     ctx->last_sims = n_sims;

@@ -197,3 +197,53 @@ def test_uncapped_cfl_tangents_vanish():
     w.n_tangents = 6
     g = _gpu(w)
     assert np.all(g["ndot_final"] == 0.0)
+
+
+# ---------------------------------------------------------------------------------------
+# k_stream (grid-wide HBM streaming kernel, forced) vs the oracle
+# ---------------------------------------------------------------------------------------
+def _stream(w, mode=oracle.MODE_DOUBLE):
+    import paper_2411_00742_b200 as pb
+    return _check(w, mode=mode, kernel=pb.KERNEL_STREAM)
+
+
+@pytest.mark.parametrize("N", [4000, 4001, 20000])
+def test_stream_c4_steps_mode(N):
+    g, o = _stream(W.c4_sweep(N, batch=3, n_steps=120))
+    assert g["info"]["kernel"] == 3
+
+
+def test_stream_landing_and_temperature_profile():
+    _stream(W.c3_cycling(N=3000, t_max=20.0, M=20, dt_max=0.05))
+    _stream(W.c2_dissolution(N=2500, t_max=30.0, M=30, dt_max=0.1))
+
+
+def test_stream_dissolution_outflow():
+    w = W.c2_dissolution(N=4000, t_max=100.0, M=25, dt_max=0.2)
+    w.n0 = W.gaussian_seed(4000, 0.3, mean=40.0, sigma=10.0, m0=0.5)[None, :]
+    w.dL = 0.3
+    w.c0 = np.array([3.0])
+    _stream(w)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_stream_tangent_lanes(P):
+    w = W.c5_ensemble(n_sims=5, N=3000, t_max=10.0, M=10, n_tangents=P)
+    _stream(w, mode=oracle.MODE_DUAL)
+
+
+def test_stream_many_sims_and_statuses():
+    w = W.c5_ensemble(n_sims=37, N=1500, t_max=5.0, M=5, n_tangents=0)
+    w.c0 = w.c0.copy(); w.c0[3] = 0.001        # infeasible
+    w.max_steps = 40                           # some sims hit MAXSTEPS
+    _stream(w)
+
+
+def test_stream_matches_resident():
+    import paper_2411_00742_b200 as pb
+    w = W.c5_ensemble(n_sims=6, N=2000, t_max=30.0, M=30, n_tangents=4)
+    a = _gpu(w, kernel=pb.KERNEL_RESIDENT)
+    b = _gpu(w, kernel=pb.KERNEL_STREAM)
+    assert np.array_equal(a["steps"], b["steps"])
+    _cmp_samples(a, b)
+    _cmp_n(a, dict(b, status=b["status"]))

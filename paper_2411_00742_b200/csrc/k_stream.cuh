@@ -29,21 +29,31 @@
 namespace pbe {
 
 constexpr int STREAM_MAXS = 8;      // simulations one CTA may touch
-constexpr int STREAM_NT = 256;      // threads per CTA
+constexpr int STREAM_NWC = 8;       // compute warps per CTA
+constexpr int STREAM_NT = 32 * (STREAM_NWC + 1);   // + 1 producer (TMA) warp
 template <int V> struct StreamCfg {
-    static constexpr int K = V <= 3 ? 4 : 2;        // consecutive bins per thread per pass
-    static constexpr int MINB = V == 1 ? 2 : 1;     // CTAs per SM (register budget)
+    static constexpr int K = V <= 3 ? 4 : 2;         // consecutive bins per thread per pass
+    static constexpr int MINB = V == 1 ? 2 : 1;      // CTAs per SM (register budget)
+    static constexpr int STAGES = V == 1 ? 3 : 2;    // smem pipeline depth
 };
+// Tile size: a function of N and V only, so a simulation's partial-sum order (and hence
+// its result, bitwise) never depends on the batch it runs in.
+__host__ __device__ inline int stream_tile(int N, int V) {
+    int tb = 256;
+    const int cap = V == 1 ? 4096 : 1024;
+    while (tb < cap && tb * 256 < N) tb <<= 1;
+    return tb;
+}
 
 struct StreamParams {
     KParams kp;
     double* buf0;           // [S][V][pitch]
     double* buf1;
     long long pitch;        // doubles per (sim, variable) row, >= N + 4, multiple of 4
-    int TB;                 // bins per tile (multiple of 4 * STREAM_NT... or of 4)
+    int TB;                 // bins per tile (stream_tile(N, V))
     int T_sim;              // tiles per simulation
     long long n_tiles;      // S * T_sim
-    double* part;           // [S][T_sim][5][V]
+    double* part;           // [S][T_sim][NWC][5][V] per-warp tile partials (slot 4: negative flag)
     unsigned* bar;          // [2]: arrive count, generation
     int* active;            // [3] rotating counters of simulations still marching
     int* final_buf;         // [S] buffer (0/1) holding each simulation's final state
@@ -59,6 +69,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
@@ -105,18 +118,98 @@ struct SimCoef {
     int active, sample;         // march this step / sample step (all moments)
 };
 
+// One thread's K bins of a tile: fluxes of K+1 faces from the smem window, update, moment
+// partials, 16-byte stores.  NEG = (C < 0) (direction is uniform per tile).
+template <int P, int K, bool NEG>
+__device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int RS, int g0, int nb, int i_base,
+                                            const SimCoef<P>& cf, bool vl, bool sample, double L_half, double dL,
+                                            double* __restrict__ drow, long long pitch,
+                                            double (&acc)[4][1 + P], bool& neg) {
+    constexpr int V = 1 + P;
+    constexpr int PP = P > 0 ? P : 1;
+    const double C = cf.C, kap2 = cf.kap2, beta2 = cf.beta2;
+    // window x[v][0..K+3] = bins g0-2 .. g0+K+1 of the tile (smem row index g0 .. g0+K+3)
+    double x[V][K + 4];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const double2* w2 = reinterpret_cast<const double2*>(sb + (size_t)v * RS + g0);
+#pragma unroll
+        for (int q = 0; q < (K + 4) / 2; ++q) { const double2 d = w2[q]; x[v][2 * q] = d.x; x[v][2 * q + 1] = d.y; }
+    }
+    double F[K + 1], Fd[K + 1][PP];
+#pragma unroll
+    for (int f = 2; f <= K + 2; ++f) {       // face between window cells f-1 | f
+        const int u = NEG ? f : f - 1;
+        const int ja = NEG ? f + 1 : f - 1;
+        const double a = x[0][ja] - x[0][ja - 1], b = x[0][f] - x[0][f - 1];
+        double h = 0.0, qa = 0.0, qb = 0.0;
+        if (vl) psi_half_d(a, b, h, qa, qb);
+        const double nup = x[0][u];
+        F[f - 2] = fma(C, nup, kap2 * h);
+        if (P > 0) {
+            const double gq = fma(beta2, h, nup), pak = kap2 * qa, pbk = kap2 * qb;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double ad = x[1 + p][ja] - x[1 + p][ja - 1], bd = x[1 + p][f] - x[1 + p][f - 1];
+                Fd[f - 2][p] = fma(cf.Cd[p], gq, fma(C, x[1 + p][u], fma(pak, ad, pbk * bd)));
+            }
+        }
+    }
+    double y[V][K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double nn = x[0][k + 2] - (F[k + 1] - F[k]);
+        neg |= (nn < 0.0);
+        y[0][k] = nn;
+#pragma unroll
+        for (int p = 0; p < P; ++p) y[1 + p][k] = x[1 + p][k + 2] - (Fd[k + 1][p] - Fd[k][p]);
+    }
+    // moment partials (mu3 every step; all moments on sample steps); bins >= nb excluded
+    const bool full = g0 + K <= nb;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double Lc = fma((double)(i_base + g0 + k), dL, L_half);
+        const double w1 = dL * Lc, w2 = w1 * Lc, w3 = w2 * Lc;
+        const bool in = full || (g0 + k < nb);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const double yv = in ? y[v][k] : 0.0;
+            acc[3][v] = fma(w3, yv, acc[3][v]);
+            if (sample) {
+                acc[0][v] = fma(dL, yv, acc[0][v]);
+                acc[1][v] = fma(w1, yv, acc[1][v]);
+                acc[2][v] = fma(w2, yv, acc[2][v]);
+            }
+        }
+    }
+    // 16-byte stores (row index of tile bin g0 is i_base + g0 + 2: 16-byte aligned)
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        double* d1 = drow + (size_t)v * pitch + g0;
+        if (full) {
+            double2* d2 = reinterpret_cast<double2*>(d1);
+#pragma unroll
+            for (int q = 0; q < K / 2; ++q) d2[q] = make_double2(y[v][2 * q], y[v][2 * q + 1]);
+        } else {
+            for (int k = 0; k < K && g0 + k < nb; ++k) d1[k] = y[v][k];
+        }
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(const StreamParams sp) {
     constexpr int V = 1 + P;
-    constexpr int PP = P > 0 ? P : 1;
     constexpr int K = StreamCfg<V>::K;
+    constexpr int STG = StreamCfg<V>::STAGES;
+    constexpr int NWC = STREAM_NWC;
     const KParams& kp = sp.kp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = STREAM_NT / 32;
+    const bool producer = (warp == NWC);
     const int N = kp.N, TB = sp.TB;
     const int RS = TB + 4;                          // smem row (tile + halos), doubles
     const bool steps_mode = kp.n_steps > 0;
     const unsigned G = gridDim.x;
+    const double L_half = kp.L_lo + 0.5 * kp.dL;
 
     // static tile range of this CTA
     const long long t_lo = (sp.n_tiles * blockIdx.x) / G;
@@ -125,10 +218,8 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
     const int ns = (t_hi > t_lo) ? (int)((t_hi - 1) / sp.T_sim) - s_lo + 1 : 0;
 
     extern __shared__ __align__(128) double smem[];
-    double* stage[2] = {smem, smem + (size_t)V * RS};
-    __shared__ __align__(8) unsigned long long s_mbar[2];
+    __shared__ __align__(8) unsigned long long s_full[STG], s_empty[STG];
     __shared__ SimCoef<P> s_coef[STREAM_MAXS];
-    __shared__ double s_red[NW][5][V];
     __shared__ double s_clip[STREAM_MAXS];
 
     // per-simulation scalar state: primal per slot (lane 0 copy), tangent per (slot, lane)
@@ -137,30 +228,12 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
     __shared__ SimPrimal s_sp[STREAM_MAXS];
     __shared__ SimTan s_st[STREAM_MAXS][32];
 
-    if (tid == 0) { mbar_init(&s_mbar[0], 1); mbar_init(&s_mbar[1], 1); }
+    if (tid == 0) {
+        for (int i = 0; i < STG; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], NWC); }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // ---- tile bookkeeping ---------------------------------------------------------------
-    auto tile_src = [&](long long t, int step_parity, int& s, int& j, int& b0, int& nb) {
-        s = (int)(t / sp.T_sim);
-        j = (int)(t - (long long)s * sp.T_sim);
-        b0 = j * TB;
-        nb = min(TB, N - b0);
-        (void)step_parity;
-    };
-    // issue the bulk loads of tile t (all V rows) into stage st
-    auto issue = [&](long long t, int st, const double* src) {
-        int s, j, b0, nb;
-        tile_src(t, 0, s, j, b0, nb);
-        const unsigned n_el = (unsigned)((nb + 4 + 1) & ~1);        // even -> 16-byte multiple
-        mbar_expect_tx(&s_mbar[st], n_el * 8u * V);
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            bulk_g2s(stage[st] + (size_t)v * RS, src + ((size_t)s * V + v) * sp.pitch + b0, n_el * 8u, &s_mbar[st]);
-    };
-
-    // ---- scalar state init (one warp per simulation slot) ------------------------------
     const int pl = lane < kp.P ? lane : -1;
     auto kinetics = [&](int slot, int s, SimPrimal& W, SimTan& T) -> bool {
         const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl, kp.n_params, kp.n_params + kp.n_sol};
@@ -185,25 +258,56 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         return true;
     };
     auto set_inactive = [&](int slot) {
-        if (lane == 0) { s_coef[slot].active = 0; s_coef[slot].sample = 0; s_coef[slot].C = 0.0;
-                         s_coef[slot].kap2 = 0.0; s_coef[slot].beta2 = 0.0; }
+        if (lane == 0) { s_coef[slot].active = 0; s_coef[slot].sample = 0; }
     };
-
-    // mu3(n0) of every simulation of this CTA: partials of step "-1" are not available, so
-    // sum the initial buffer directly (each slot warp, fixed order over bins).
-    if (warp < ns) {
-        const int slot = warp, s = s_lo + slot;
-        const double* row = sp.buf0 + (size_t)s * V * sp.pitch + 2;
-        double a = 0.0;
-        for (int i = lane; i < N; i += 32) {
-            const double Lc = fma((double)i, kp.dL, kp.L_lo + 0.5 * kp.dL);
-            a = fma(kp.dL * Lc * Lc * Lc, row[i], a);
+    // totals of simulation s from the per-(tile, warp) partials, fixed order (deterministic):
+    // lane l sums entries e = l, l + 32, ...; then a fixed xor tree per value.
+    auto sim_totals = [&](int s, bool sample, double (&tot)[4], double (&totd)[4], double& badf) {
+        const double* pt = sp.part + (size_t)s * sp.T_sim * NWC * 5 * V;
+        const int ne = sp.T_sim * NWC;
+        double a[4][V];
+#pragma unroll
+        for (int km = 0; km < 4; ++km)
+#pragma unroll
+            for (int v = 0; v < V; ++v) a[km][v] = 0.0;
+        double bf = 0.0;
+        for (int e = lane; e < ne; e += 32) {
+            const double* q = pt + (size_t)e * 5 * V;
+#pragma unroll
+            for (int km = 0; km < 4; ++km)
+                if (km == 3 || sample) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) a[km][v] += q[km * V + v];
+                }
+            bf += q[4 * V];
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);   // fixed tree
+        for (int km = 0; km < 4; ++km) {
+            tot[km] = 0.0; totd[km] = 0.0;
+            if (km == 3 || sample) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) a[km][v] += __shfl_xor_sync(0xffffffffu, a[km][v], off);
+                tot[km] = a[km][0];
+#pragma unroll
+                for (int p = 0; p < P; ++p) if (p == pl) totd[km] = a[km][1 + p];
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) bf += __shfl_xor_sync(0xffffffffu, bf, off);
+        badf = bf;
+    };
+
+    // ---- scalar state init (one warp per simulation slot); mu3(n0) from the load kernel's
+    //      per-tile partials (same layout and order as a step) ----------------------------
+    if (warp < ns) {
+        const int slot = warp, s = s_lo + slot;
+        double tot[4], totd[4], badf;
+        sim_totals(s, false, tot, totd, badf);
         SimPrimal W{};
         SimTan T{};
-        W.c = kp.c0[s]; W.t = 0.0; W.mu3p = a; W.dt = 0.0; W.loss = 0.0; W.rms_c = 1.0; W.rms_L = 1.0;
+        W.c = kp.c0[s]; W.t = 0.0; W.mu3p = tot[3]; W.dt = 0.0; W.loss = 0.0; W.rms_c = 1.0; W.rms_L = 1.0;
         W.nstep = 0; W.m = 0; W.status = ST_OK; W.landing = 0; W.go = 1;
         T.c = T.t = T.mu3p = T.dt = T.gacc = 0.0;
         if (kp.target) {
@@ -221,10 +325,7 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         if (kp.max_steps <= 0) { W.status = ST_MAXSTEPS; W.go = 0; }
         if (W.go && !kinetics(slot, s, W, T)) W.go = 0;
         if (W.go) {
-            if (lane == 0) {
-                s_coef[slot].active = 1;
-                s_coef[slot].sample = W.landing || (steps_mode && kp.n_steps == 1);
-            }
+            if (lane == 0) { s_coef[slot].active = 1; s_coef[slot].sample = W.landing || (steps_mode && kp.n_steps == 1); }
         } else {
             set_inactive(slot);
         }
@@ -237,140 +338,102 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
     unsigned gen = 0;
     long long n = 0;
     int src_sel = 0;
-    unsigned phase[2] = {0u, 0u};
+    unsigned long long qq = 0;          // running tile counter (stage = qq % STG, phase = (qq / STG) & 1)
+    const bool vl = kp.limiter == LIM_VANLEER;
+    auto tile_active = [&](long long t) { return s_coef[(int)(t / sp.T_sim) - s_lo].active != 0; };
+    auto next_active = [&](long long t) { while (t < t_hi && !tile_active(t)) ++t; return t; };
     while (true) {
         const double* src = src_sel ? sp.buf1 : sp.buf0;
         double* dst = src_sel ? sp.buf0 : sp.buf1;
-        // ---- tiles ----------------------------------------------------------------------
-        // skip leading/trailing tiles of inactive simulations
-        bool first_issued = false;
-        auto tile_active = [&](long long t) { return s_coef[(int)(t / sp.T_sim) - s_lo].active != 0; };
-        long long t_next = t_lo;
-        while (t_next < t_hi && !tile_active(t_next)) ++t_next;
-        if (tid == 0 && t_next < t_hi) { asm volatile("fence.proxy.async.global;" ::: "memory"); issue(t_next, 0, src); }
-        first_issued = t_next < t_hi;
-        int st = 0;
-        for (long long t = t_next; first_issued && t < t_hi;) {
-            // find the next active tile to prefetch
-            long long tn = t + 1;
-            while (tn < t_hi && !tile_active(tn)) ++tn;
-            if (tid == 0 && tn < t_hi) issue(tn, st ^ 1, src);
-            mbar_wait(&s_mbar[st], phase[st]);
-            phase[st] ^= 1u;
-
-            int s, j, b0, nb;
-            tile_src(t, 0, s, j, b0, nb);
-            const int slot = s - s_lo;
-            const SimCoef<P>& cf = s_coef[slot];
-            const double C = cf.C, kap2 = cf.kap2, beta2 = cf.beta2;
-            const bool sample = cf.sample != 0;
-            const double clip_thr = s_clip[slot];
-            double Cd[PP];
+        const unsigned long long q0 = qq;
+        if (producer) {
+            // ---- TMA producer: one elected lane streams the active tiles through the stages ----
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                unsigned long long q = q0;
+                for (long long t = next_active(t_lo); t < t_hi; t = next_active(t + 1), ++q) {
+                    const int st = (int)(q % STG);
+                    if (q >= STG) mbar_wait(&s_empty[st], (unsigned)(((q / STG) - 1) & 1));
+                    const int s = (int)(t / sp.T_sim), j = (int)(t - (long long)s * sp.T_sim);
+                    const int b0 = j * TB, nb = min(TB, N - b0);
+                    const unsigned n_el = (unsigned)((nb + 4 + 1) & ~1);   // even -> 16-byte multiple
+                    mbar_expect_tx(&s_full[st], n_el * 8u * V);
 #pragma unroll
-            for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? cf.Cd[p] : 0.0;
-            const double* sb = stage[st];
-
-            double acc[4][V];
-#pragma unroll
-            for (int km = 0; km < 4; ++km)
-#pragma unroll
-                for (int v = 0; v < V; ++v) acc[km][v] = 0.0;
-            bool bad = false;
-            const bool vl = kp.limiter == LIM_VANLEER;
-
-            for (int g0 = tid * K; g0 < nb; g0 += STREAM_NT * K) {
-                // window x[v][0..K+3] = bins b0+g0-2 .. b0+g0+K+1 (smem row index g0 .. g0+K+3)
-                double x[V][K + 4];
-#pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    const double2* w2 = reinterpret_cast<const double2*>(sb + (size_t)v * RS + g0);
-#pragma unroll
-                    for (int q = 0; q < (K + 4) / 2; ++q) { const double2 d = w2[q]; x[v][2 * q] = d.x; x[v][2 * q + 1] = d.y; }
+                    for (int v = 0; v < V; ++v)
+                        bulk_g2s(smem + ((size_t)st * V + v) * RS, src + ((size_t)s * V + v) * sp.pitch + b0,
+                                 n_el * 8u, &s_full[st]);
                 }
-                // face between window cells (f-1, f), f = 2..K+2  (bins b0+g0+f-3 | b0+g0+f-2)
-                double F[K + 1], Fd[K + 1][PP];
+            }
+            // the producer warp counts the same tiles as the consumers
+            for (long long t = next_active(t_lo); t < t_hi; t = next_active(t + 1)) ++qq;
+        } else {
+            // ---- consumers --------------------------------------------------------------------
+            for (long long t = next_active(t_lo); t < t_hi; t = next_active(t + 1), ++qq) {
+                const int st = (int)(qq % STG);
+                mbar_wait(&s_full[st], (unsigned)((qq / STG) & 1));
+                const int s = (int)(t / sp.T_sim), j = (int)(t - (long long)s * sp.T_sim);
+                const int b0 = j * TB, nb = min(TB, N - b0);
+                const int slot = s - s_lo;
+                const SimCoef<P>& cf = s_coef[slot];
+                const bool sample = cf.sample != 0;
+                const double* sb = smem + (size_t)st * V * RS;
+                double* drow = dst + (size_t)s * V * sp.pitch + b0 + 2;
+                double acc[4][V];
 #pragma unroll
-                for (int f = 2; f <= K + 2; ++f) {
-                    const int u = C >= 0.0 ? f - 1 : f;
-                    const int ja = C >= 0.0 ? f - 1 : f + 1;
-                    const double a = x[0][ja] - x[0][ja - 1], b = x[0][f] - x[0][f - 1];
-                    double h = 0.0, qa = 0.0, qb = 0.0;
-                    if (vl) psi_half_d(a, b, h, qa, qb);
-                    const double nup = x[0][u];
-                    F[f - 2] = fma(C, nup, kap2 * h);
-                    const double gq = fma(beta2, h, nup), pak = kap2 * qa, pbk = kap2 * qb;
+                for (int km = 0; km < 4; ++km)
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        const double ad = x[1 + p][ja] - x[1 + p][ja - 1], bd = x[1 + p][f] - x[1 + p][f - 1];
-                        Fd[f - 2][p] = fma(Cd[p], gq, fma(C, x[1 + p][u], fma(pak, ad, pbk * bd)));
-                    }
+                    for (int v = 0; v < V; ++v) acc[km][v] = 0.0;
+                bool neg = false;
+                if (cf.C >= 0.0) {
+                    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
+                        stream_bins<P, K, false>(sb, RS, g0, nb, b0, cf, vl, sample, L_half, kp.dL, drow, sp.pitch, acc, neg);
+                } else {
+                    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
+                        stream_bins<P, K, true>(sb, RS, g0, nb, b0, cf, vl, sample, L_half, kp.dL, drow, sp.pitch, acc, neg);
                 }
-                // update bins k = 0..K-1 (window cell k + 2)
-                double y[V][K];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[st]);           // stage free for the producer
+                // round-off clip (R-17), rare: fix the stored values of this warp's bins
+                bool bad = false;
+                if (__any_sync(0xffffffffu, neg)) {
+                    const double thr = s_clip[slot];
+                    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
+                        for (int k = 0; k < K && g0 + k < nb; ++k) {
+                            const double nn = drow[g0 + k];
+                            if (nn < 0.0) {
+                                if (nn >= -thr) {
+                                    // zero the bin and its tangents; remove it from the partials
+                                    const double Lc = fma((double)(b0 + g0 + k), kp.dL, L_half);
+                                    const double w1 = kp.dL * Lc, w2 = w1 * Lc, w3 = w2 * Lc;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int i = b0 + g0 + k;
-                    const double nn = x[0][k + 2] - (F[k + 1] - F[k]);
-                    const bool zero = (i >= N) || (nn < 0.0 && nn >= -clip_thr);
-                    bad |= (nn < -clip_thr) && (i < N);
-                    y[0][k] = zero ? 0.0 : nn;
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        const double nd = x[1 + p][k + 2] - (Fd[k + 1][p] - Fd[k][p]);
-                        y[1 + p][k] = zero ? 0.0 : nd;
-                    }
-                    const double Lc = fma((double)i, kp.dL, kp.L_lo + 0.5 * kp.dL);
-                    double w = kp.dL;
-#pragma unroll
-                    for (int km = 0; km < 4; ++km) {
-                        if (km == 3 || sample) {
-#pragma unroll
-                            for (int v = 0; v < V; ++v) acc[km][v] = fma(w, y[v][k], acc[km][v]);
+                                    for (int v = 0; v < V; ++v) {
+                                        const double yv = drow[(size_t)v * sp.pitch + g0 + k];
+                                        acc[3][v] -= w3 * yv;
+                                        if (sample) { acc[0][v] -= kp.dL * yv; acc[1][v] -= w1 * yv; acc[2][v] -= w2 * yv; }
+                                        drow[(size_t)v * sp.pitch + g0 + k] = 0.0;
+                                    }
+                                } else {
+                                    bad = true;
+                                }
+                            }
                         }
-                        w *= Lc;
-                    }
                 }
-                // coalesced 16-byte stores (row index of bin b0+g0 is b0+g0+2: 16-byte aligned)
+                // per-warp tile partials
+                double* pt = sp.part + (((size_t)s * sp.T_sim + j) * NWC + warp) * 5 * V;
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    double2* d2 = reinterpret_cast<double2*>(dst + ((size_t)s * V + v) * sp.pitch + b0 + g0 + 2);
-                    if (g0 + K <= nb) {
-#pragma unroll
-                        for (int q = 0; q < K / 2; ++q) d2[q] = make_double2(y[v][2 * q], y[v][2 * q + 1]);
-                    } else {
-                        double* d1 = dst + ((size_t)s * V + v) * sp.pitch + b0 + g0 + 2;
-                        for (int k = 0; k < K && g0 + k < nb; ++k) d1[k] = y[v][k];
-                    }
-                }
-            }
-            // ---- tile partials: warp transpose-reduce, then warp 0 sums the warps ------------
-#pragma unroll
-            for (int km = 0; km < 4; ++km) {
-                if (km == 3 || sample) {
-                    double r[V];
-#pragma unroll
-                    for (int v = 0; v < V; ++v) r[v] = acc[km][v];
-                    warp_transpose_reduce<V>(r, lane);
-                    const int idx = reduce_index<V>(lane);
-                    if (idx < V) s_red[warp][km][idx] = r[0];
-                }
-            }
-            const int bad_any = __syncthreads_or(bad);
-            if (warp == 0) {
-                double* pt = sp.part + (((size_t)s * sp.T_sim + j) * 5) * V;
-                for (int e = lane; e < 4 * V; e += 32) {
-                    const int km = e / V, v = e - km * V;
+                for (int km = 0; km < 4; ++km) {
                     if (km == 3 || sample) {
-                        double a = 0.0;
-                        for (int w = 0; w < NW; ++w) a += s_red[w][km][v];
-                        pt[km * V + v] = a;
+                        double r[V];
+#pragma unroll
+                        for (int v = 0; v < V; ++v) r[v] = acc[km][v];
+                        warp_transpose_reduce<V>(r, lane);
+                        const int idx = reduce_index<V>(lane);
+                        if (idx < V) pt[km * V + idx] = r[0];
                     }
                 }
+                const bool bad_any = __any_sync(0xffffffffu, bad);
                 if (lane == 0) pt[4 * V] = bad_any ? 1.0 : 0.0;
             }
-            __syncthreads();       // stage st and s_red free for reuse
-            st ^= 1;
-            t = tn;
         }
 
         // ---- grid barrier + active count ------------------------------------------------------
@@ -394,20 +457,8 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
             SimPrimal W = s_sp[slot];
             SimTan T = s_st[slot][lane];
             const bool sample = s_coef[slot].sample != 0;
-            double tot[4] = {0.0, 0.0, 0.0, 0.0}, totd[4] = {0.0, 0.0, 0.0, 0.0};
-            double badf = 0.0;
-            const double* pt = sp.part + ((size_t)s * sp.T_sim * 5) * V;
-            for (int jt = 0; jt < sp.T_sim; ++jt) {
-                const double* q = pt + (size_t)jt * 5 * V;
-#pragma unroll
-                for (int km = 0; km < 4; ++km) {
-                    if (km == 3 || sample) {
-                        tot[km] += q[km * V];
-                        if (pl >= 0) totd[km] += q[km * V + 1 + pl];
-                    }
-                }
-                badf += q[4 * V];
-            }
+            double tot[4], totd[4], badf;
+            sim_totals(s, sample, tot, totd, badf);
             const D1 mu3n = mk(tot[3], totd[3]);
             const D1 c = mk(W.c, T.c), mu3p = mk(W.mu3p, T.mu3p);
             const D1 cn = c - kp.rho_kv * (mu3n - mu3p);
@@ -476,22 +527,43 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
     }
 }
 
-// n0 (caller layout [S or 1][N]) -> padded buffer 0; tangent rows 0; per-sim max(n0) bits.
+// n0 (caller layout [S or 1][N]) -> padded buffer 0; tangent rows 0; per-sim max(n0) bits;
+// mu3(n0) partial of every tile in the step-partial layout (warp slot 0, fixed order).
+// Grid (T_sim, S), 256 threads: one CTA per tile.
 template <int V>
-__global__ void k_stream_load(const double* __restrict__ n0, long long n0_stride, int N, int S,
-                              double* __restrict__ buf, long long pitch, unsigned long long* nscale_bits) {
-    const int s = blockIdx.y;
-    double m = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) k_stream_load(const double* __restrict__ n0, long long n0_stride, int N, int S,
+                              double* __restrict__ buf, long long pitch, unsigned long long* nscale_bits,
+                              int TB, int T_sim, double* __restrict__ part, double L_lo, double dL) {
+    const int s = blockIdx.y, j = blockIdx.x;
+    const int b0 = j * TB, nb = min(TB, N - b0);
+    double m = 0.0, a3 = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        const int i = b0 + k;
         const double v = n0[(size_t)s * n0_stride + i];
         buf[(size_t)s * V * pitch + 2 + i] = v;
 #pragma unroll
         for (int p = 1; p < V; ++p) buf[((size_t)s * V + p) * pitch + 2 + i] = 0.0;
         m = fmax(m, v);
+        const double Lc = fma((double)i, dL, L_lo + 0.5 * dL);
+        a3 = fma(dL * Lc * Lc * Lc, v, a3);
     }
+    __shared__ double s_a[8];
+    __shared__ double s_m[8];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if ((threadIdx.x & 31) == 0) atomicMax(nscale_bits + s, (unsigned long long)__double_as_longlong(m));
+    for (int off = 16; off > 0; off >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+    }
+    if ((threadIdx.x & 31) == 0) { s_a[threadIdx.x >> 5] = a3; s_m[threadIdx.x >> 5] = m; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, mm = 0.0;
+        for (int w = 0; w < 8; ++w) { t += s_a[w]; mm = fmax(mm, s_m[w]); }
+        double* pt = part + ((size_t)s * T_sim + j) * STREAM_NWC * 5 * V;
+        for (int e = 0; e < STREAM_NWC * 5 * V; ++e) pt[e] = 0.0;
+        pt[3 * V] = t;
+        atomicMax(nscale_bits + s, (unsigned long long)__double_as_longlong(mm));
+    }
 }
 
 // final state (buffer chosen per simulation) -> caller n_final [S][N] / ndot_final [S][P][N]

@@ -113,7 +113,8 @@ const ResidentVariant kResident[] = {
 struct StreamVariant {
     int P;
     const void* fn;
-    void (*load)(const double*, long long, int, int, double*, long long, unsigned long long*);
+    void (*load)(const double*, long long, int, int, double*, long long, unsigned long long*, int, int, double*,
+                 double, double);
     void (*store)(const double*, const double*, const int*, int, int, long long, double*, double*);
 };
 #define SV(P) StreamVariant{P, (const void*)&pbe::k_stream<P>, &pbe::k_stream_load<1 + P>, &pbe::k_stream_store<1 + P>}
@@ -163,11 +164,10 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     const long long pitch = ((long long)N + 4 + 3) / 4 * 4;
     int dev = ctx->device, sms = 0;
     CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // occupancy of the cooperative kernel (smem depends on TB: pick TB first for 2 CTAs/SM)
-    const long long work = (long long)S * N;
-    int TB = 4096;
-    while (TB > 256 && work / TB < 4LL * 2 * sms) TB >>= 1;
-    const size_t smem = (size_t)2 * V * (TB + 4) * sizeof(double);
+    // tile size depends on N and V only (batch-independent partial-sum order)
+    const int TB = pbe::stream_tile(N, V);
+    const int stages = V == 1 ? pbe::StreamCfg<1>::STAGES : pbe::StreamCfg<3>::STAGES;
+    const size_t smem = (size_t)stages * V * (TB + 4) * sizeof(double);
     CUDA_TRY(ctx, cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sv.fn, pbe::STREAM_NT, smem));
@@ -182,7 +182,7 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
 
     const size_t buf_el = (size_t)S * V * pitch;
     CUDA_TRY(ctx, ctx->sbuf.ensure(2 * buf_el * sizeof(double)));
-    CUDA_TRY(ctx, ctx->spart.ensure((size_t)S * T_sim * 5 * V * sizeof(double)));
+    CUDA_TRY(ctx, ctx->spart.ensure((size_t)S * T_sim * pbe::STREAM_NWC * 5 * V * sizeof(double)));
     CUDA_TRY(ctx, ctx->sbar.ensure(8 * sizeof(unsigned)));
     CUDA_TRY(ctx, ctx->sfinal.ensure((size_t)S * sizeof(int)));
     CUDA_TRY(ctx, ctx->snscale.ensure((size_t)S * sizeof(unsigned long long)));
@@ -192,9 +192,10 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbuf.p, 0, 2 * buf_el * sizeof(double), st));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbar.p, 0, 8 * sizeof(unsigned), st));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->snscale.p, 0, (size_t)S * sizeof(unsigned long long), st));
-    const dim3 lg((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, S);
-    sv.load<<<lg, 256, 0, st>>>(n0, n0_stride, N, S, b0, pitch, ctx->snscale.as<unsigned long long>());
+    sv.load<<<dim3(T_sim, S), 256, 0, st>>>(n0, n0_stride, N, S, b0, pitch, ctx->snscale.as<unsigned long long>(),
+                                            TB, T_sim, ctx->spart.as<double>(), kp.L_lo, kp.dL);
     CUDA_TRY(ctx, cudaGetLastError());
+    const dim3 lg((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, S);
 
     pbe::StreamParams sp{};
     sp.kp = kp;

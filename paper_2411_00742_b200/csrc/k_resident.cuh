@@ -29,6 +29,8 @@
 //  so only Cdot is lane-specific (8 FP64 ops per bin and lane).
 // =====================================================================================
 #pragma once
+#include <cooperative_groups.h>
+
 #include <type_traits>
 
 #include "pbe_device.cuh"
@@ -147,20 +149,34 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 // sample index, status) and evaluates the kinetics redundantly from the same smem partial
 // sums in the same order, so all warps take bitwise-identical decisions.  Halos, partial
 // sums and the negative-density flag are double-buffered by step parity.
-template <int P, int K, int MAXT>
+//
+// CL = true: thread-block-cluster mode (k_cluster, 10^4 - 10^5 bins).  A cluster of CS CTAs
+// (launch attribute, <= 16) marches one simulation; CTA rank r owns bins
+// [(r NT + t) K, ...).  The boundary bins of neighbouring CTAs are written straight into
+// the neighbour's ghost column through distributed shared memory, every CTA pre-reduces
+// its warps' moment partials, and the scalar phase sums the CS CTA totals over DSMEM in
+// rank order.  The one barrier per step becomes a cluster barrier.
+template <int P, int K, int MAXT, bool CL = false>
 __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
+    namespace cg = cooperative_groups;
     constexpr int V = 1 + P;
     constexpr int PP = P > 0 ? P : 1;
     static_assert(K >= 2, "K >= 2");
-    const int s = blockIdx.x / kp.G;
-    const int grp = blockIdx.x - s * kp.G;
+    const int CS = CL ? (int)cg::this_cluster().num_blocks() : 1;
+    const int rank = CL ? (int)cg::this_cluster().block_rank() : 0;
+    const int unit = blockIdx.x / CS;
+    const int s = unit / kp.G;
+    const int grp = unit - s * kp.G;
     const int lane0 = grp * P;                                 // first tangent lane of the group
     const int nl = P > 0 ? max(0, min(P, kp.P - lane0)) : 0;   // lanes of this group in use
-    const bool primal_out = (grp == 0);
+    const bool primal_out = (grp == 0) && (rank == 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
     const int N = kp.N;
-    const int i0 = tid * K;
+    const int i0 = (rank * NT + tid) * K;
+    auto block_barrier = [&]() {
+        if (CL) cg::this_cluster().sync(); else __syncthreads();
+    };
     const int HS = NT + 2;
     const int HP = 4 * V * HS;                  // doubles per halo parity
     const bool steps_mode = kp.n_steps > 0;
@@ -171,6 +187,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     __shared__ double s_red[2][32][4][V];       // [parity][warp][moment][value]
     __shared__ long long s_bad[2];              // step index that produced a negative
     __shared__ double s_nscale;
+    __shared__ double s_cta[2][4][V];           // cluster mode: this CTA's moment totals
 
     double x[V][K];
     // ---- load n0 (tangents start at 0: n0 does not depend on theta, R-20) --------------
@@ -195,6 +212,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         for (int w = 0; w < NW; ++w) m = fmax(m, s_red[0][w][0][0]);
         s_nscale = m;
     }
+    if (CL) {   // clip scale = max over the whole simulation
+        cg::this_cluster().sync();
+        if (tid == 0) {
+            double m = 0.0;
+            for (int r = 0; r < CS; ++r) m = fmax(m, *cg::this_cluster().map_shared_rank(&s_nscale, r));
+            s_red[1][0][0][0] = m;
+        }
+        cg::this_cluster().sync();
+        if (tid == 0) s_nscale = s_red[1][0][0][0];
+    }
 
     auto publish_halo = [&](int q) {
         double* h = s_halo + q * HP;
@@ -204,6 +231,33 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
             h[(1 * V + v) * HS + tid + 1] = x[v][1];
             h[(2 * V + v) * HS + tid + 1] = x[v][K - 2];
             h[(3 * V + v) * HS + tid + 1] = x[v][K - 1];
+        }
+        if (CL) {   // DSMEM: my edge bins -> the neighbour CTAs' ghost columns
+            if (tid == NT - 1 && rank + 1 < CS) {
+                double* hr = cg::this_cluster().map_shared_rank(h, rank + 1);
+#pragma unroll
+                for (int v = 0; v < V; ++v) { hr[(2 * V + v) * HS] = x[v][K - 2]; hr[(3 * V + v) * HS] = x[v][K - 1]; }
+            }
+            if (tid == 0 && rank > 0) {
+                double* hl = cg::this_cluster().map_shared_rank(h, rank - 1);
+#pragma unroll
+                for (int v = 0; v < V; ++v) { hl[(0 * V + v) * HS + NT + 1] = x[v][0]; hl[(1 * V + v) * HS + NT + 1] = x[v][1]; }
+            }
+        }
+    };
+    // cluster mode: this CTA's totals of the warp partials (fixed warp order) -> s_cta[q]
+    auto cta_totals = [&](int q, bool all_moments) {
+        if (!CL) return;
+        __syncthreads();
+        if (warp == 0) {
+            for (int e = lane; e < 4 * V; e += 32) {
+                const int km = e / V, v = e - km * V;
+                if (km == 3 || all_moments) {
+                    double a = 0.0;
+                    for (int w = 0; w < NW; ++w) a += s_red[q][w][km][v];
+                    s_cta[q][km][v] = a;
+                }
+            }
         }
     };
     // moment KM partials of all V variables, warp-reduced into s_red[q][warp][KM][*]
@@ -229,7 +283,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     const double clip_thr = 1e-12 * s_nscale;
     moment_partials(1, std::integral_constant<int, 3>{});   // mu3(n0): "step -1" outputs in parity 1
     publish_halo(1);
-    __syncthreads();
+    cta_totals(1, false);
+    block_barrier();
 
     // ---- per-warp scalar state (lane p: primal + tangent p) ------------------------------
     // Kept in smem between scalar phases (one slot per thread) so that the sweep has the
@@ -291,7 +346,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     {
         LaneScal L;
         double a = 0.0;
-        for (int w = 0; w < NW; ++w) a += s_red[1][w][3][0];
+        if (CL) {
+            for (int r = 0; r < CS; ++r) a += cg::this_cluster().map_shared_rank(&s_cta[1][3][0], r)[0];
+        } else {
+            for (int w = 0; w < NW; ++w) a += s_red[1][w][3][0];
+        }
         L.c = mk(kp.c0[s]); L.t = mk(0.0); L.mu3p = mk(a, 0.0); L.dt = mk(0.0);
         L.loss = 0.0; L.gacc = 0.0; L.rms_c = 1.0; L.rms_L = 1.0;
         L.nstep = 0; L.m = 0; L.status = ST_OK; L.landing = 0;
@@ -331,7 +390,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
             moment_partials(q, std::integral_constant<int, 2>{});
         }
         publish_halo(q);
-        __syncthreads();                         // the one barrier of the step
+        cta_totals(q, sample);
+        block_barrier();                         // the one (cluster) barrier of the step
 
         // ---- scalar phase (every warp, identical arithmetic) -----------------------------
         LaneScal L = load_ls();
@@ -340,22 +400,33 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
         for (int km = 0; km < 4; ++km) {
             if (km == 3 || sample) {
                 double a = 0.0, b = 0.0;
-                for (int w = 0; w < NW; ++w) {
-                    a += s_red[q][w][km][0];
-                    if (pl >= 0) b += s_red[q][w][km][1 + pl];
+                if (CL) {
+                    for (int r = 0; r < CS; ++r) {
+                        const double* rc = cg::this_cluster().map_shared_rank(&s_cta[q][km][0], r);
+                        a += rc[0];
+                        if (pl >= 0) b += rc[1 + pl];
+                    }
+                } else {
+                    for (int w = 0; w < NW; ++w) {
+                        a += s_red[q][w][km][0];
+                        if (pl >= 0) b += s_red[q][w][km][1 + pl];
+                    }
                 }
                 tot[km] = a; totd[km] = b;
             }
         }
         const D1 mu3n = mk(tot[3], totd[3]);
         const D1 cn = L.c - kp.rho_kv * (mu3n - L.mu3p);        // eq-discrete_mass_balance
-        if (s_bad[q] == n) { L.status = ST_NEG; go = false; }
+        bool any_bad = s_bad[q] == n;
+        if (CL)
+            for (int r = 0; r < CS; ++r) any_bad |= (*cg::this_cluster().map_shared_rank(&s_bad[q], r) == n);
+        if (any_bad) { L.status = ST_NEG; go = false; }
         else if (cn.v < 0.0) { L.status = ST_INFEAS; go = false; }
         else {
             L.c = cn; L.mu3p = mu3n;
             L.t = L.landing ? mk(kp.t_samples[L.m], 0.0) : L.t + L.dt;
             ++L.nstep;
-            if (sample && warp == 0) {
+            if (sample && warp == 0 && rank == 0) {
                 const int mr = steps_mode ? 0 : L.m;
                 double* r = kp.rec + ((size_t)s * kp.M + mr) * 6;
                 if (lane == 0 && primal_out) { r[0] = L.t.v; r[1] = L.c.v; r[2] = tot[0]; r[3] = tot[1]; r[4] = tot[2]; r[5] = tot[3]; }
@@ -382,7 +453,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     }
 
     // ---- epilogue -----------------------------------------------------------------------
-    if (kp.n_final && primal_out) {
+    if (kp.n_final && grp == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) { const int i = i0 + k; if (i < N) kp.n_final[(size_t)s * N + i] = x[0][k]; }
     }
@@ -408,8 +479,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
             kp.steps[s] = L.nstep;
             if (kp.loss) kp.loss[s] = (has_target && ok) ? L.loss : qnan;
         }
-        if (pl >= 0 && kp.grad) kp.grad[(size_t)s * kp.P + lane0 + pl] = (has_target && ok) ? L.gacc : qnan;
+        if (pl >= 0 && kp.grad && rank == 0) kp.grad[(size_t)s * kp.P + lane0 + pl] = (has_target && ok) ? L.gacc : qnan;
     }
+    if (CL) cg::this_cluster().sync();   // keep this CTA's smem alive for DSMEM readers
 }
 
 }  // namespace pbe

@@ -109,6 +109,30 @@ const ResidentVariant kResident[] = {
 };
 #undef RV
 
+// k_resident<P, K, MAXT, true> cluster variants (cluster size chosen at launch, <= 16)
+#define CV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T, true>}
+const ResidentVariant kCluster[] = {
+    CV(0, 8, 512), CV(0, 16, 512),
+    CV(2, 4, 512), CV(2, 8, 512),
+    CV(4, 4, 512), CV(4, 8, 256),
+    CV(8, 4, 256), CV(8, 8, 256),
+};
+#undef CV
+// smallest cluster (then smallest K) whose CTAs cover N bins
+const ResidentVariant* pick_cluster(int N, int P, int* cs) {
+    const int Pi = P == 0 ? 0 : (P <= 2 ? 2 : (P <= 4 ? 4 : (P <= 8 ? 8 : -1)));
+    for (int c = 2; c <= 16; c *= 2) {
+        const ResidentVariant* best = nullptr;
+        for (const auto& v : kCluster) {
+            if (v.P != Pi) continue;
+            if ((long long)v.K * v.maxt * c < N) continue;
+            if (!best || v.K < best->K) best = &v;
+        }
+        if (best) { *cs = c; return best; }
+    }
+    return nullptr;
+}
+
 // k_stream<P> variants: lanes per launch (the tangent lanes of a simulation are never split)
 struct StreamVariant {
     int P;
@@ -376,10 +400,12 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     int groups = 1;
     const ResidentVariant* rv = pick_resident(N, P, ctx->group_max, &groups);
     const StreamVariant* sv = pick_stream(P);
+    int cs = 1;
+    const ResidentVariant* cv = pick_cluster(N, P, &cs);
     int kind = cf.kernel;
-    if (kind == PBE_KERNEL_AUTO) kind = rv ? PBE_KERNEL_RESIDENT : PBE_KERNEL_STREAM;
-    if (kind == PBE_KERNEL_CLUSTER)
-        return fail(ctx, PBE_ERR_ARG, "kernel variant %d not available in this build", kind);
+    if (kind == PBE_KERNEL_AUTO) kind = rv ? PBE_KERNEL_RESIDENT : (cv ? PBE_KERNEL_CLUSTER : PBE_KERNEL_STREAM);
+    if (kind == PBE_KERNEL_CLUSTER && !cv)
+        return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit a 16-CTA cluster", N, P);
     if (kind == PBE_KERNEL_RESIDENT && !rv)
         return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit the resident kernel", N, P);
     if (kind == PBE_KERNEL_STREAM && !sv)
@@ -436,6 +462,33 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
         ctx->info.ctas = n_sims * groups;
         ctx->info.cluster = 1;
         ctx->info.bins_per_thread = rv->K;
+    } else if (kind == PBE_KERNEL_CLUSTER) {
+        const int nt = ((N + cv->K * cs - 1) / (cv->K * cs) + 31) / 32 * 32;
+        const size_t smem = resident_smem(*cv, nt);
+        CUDA_TRY(ctx, cudaFuncSetAttribute(cv->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (cs > 8) CUDA_TRY(ctx, cudaFuncSetAttribute(cv->fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        kp.G = 1;                                   // tangent lanes are not split in cluster mode
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(n_sims * cs);
+        lc.blockDim = dim3(nt);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+        CUDA_TRY(ctx, cudaLaunchKernelEx(&lc, cv->fn, kp));
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+        ctx->info.kernel = PBE_KERNEL_CLUSTER;
+        ctx->info.launches = 1;
+        ctx->info.threads_per_cta = nt;
+        ctx->info.ctas = n_sims * cs;
+        ctx->info.cluster = cs;
+        ctx->info.bins_per_thread = cv->K;
     } else {
         pbe_status r = launch_stream(ctx, *sv, kp, n_sims, n0_dev, n0_stride, st);
         if (r != PBE_OK) return r;

@@ -247,3 +247,36 @@ def test_stream_matches_resident():
     assert np.array_equal(a["steps"], b["steps"])
     _cmp_samples(a, b)
     _cmp_n(a, dict(b, status=b["status"]))
+
+
+# ---------------------------------------------------------------------------------------
+# k_cluster (thread-block cluster + DSMEM mode of the resident kernel, forced) vs the oracle
+# ---------------------------------------------------------------------------------------
+def _cluster(w, mode=oracle.MODE_DOUBLE):
+    import paper_2411_00742_b200 as pb
+    g, o = _check(w, mode=mode, kernel=pb.KERNEL_CLUSTER)
+    assert g["info"]["kernel"] == 2 and g["info"]["cluster"] >= 2
+    return g, o
+
+
+@pytest.mark.parametrize("N", [9000, 12001, 40000])
+def test_cluster_c4_steps_mode(N):
+    _cluster(W.c4_sweep(N, batch=2, n_steps=100))
+
+
+def test_cluster_landing_dissolution_and_cycling():
+    _cluster(W.c3_cycling(N=10000, t_max=5.0, M=5, dt_max=0.02))
+    _cluster(W.c2_dissolution(N=10000, t_max=20.0, M=20, dt_max=0.1))
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_cluster_tangents(P):
+    w = W.c5_ensemble(n_sims=3, N=5000, t_max=6.0, M=6, n_tangents=P)
+    _cluster(w, mode=oracle.MODE_DUAL)
+
+
+def test_cluster_statuses():
+    w = W.c5_ensemble(n_sims=6, N=9000, t_max=4.0, M=4, n_tangents=0)
+    w.c0 = w.c0.copy(); w.c0[2] = 0.001
+    w.max_steps = 30
+    _cluster(w)

@@ -82,7 +82,7 @@ def replicate_single(w, world: int):
 def flops_per_bin_update(limiter: int, P: int) -> float:
     if limiter == W.LIM_UPWIND:
         primal = 5.0          # F = C n_up (1), update (2), mu3 FMA (2)
-        lane = 9.0            # Fdot = Cdot n_up + C ndot_up (3), update (2), mu3dot (2), ... (2 for d-free form)
+        lane = 7.0            # Fdot = Cdot n_up + C ndot_up (3), update (2), mu3dot (2)
         return primal + lane * P
     primal = 12.0             # d (1), psi = 2ab/(a+b) (4), F = C n_up + kap psi (3), update (2), mu3 (2)
     face_t = 8.0 if P else 0  # psi partials pa, pb (6) + g = n_up + beta psi (2), once per face
@@ -201,17 +201,16 @@ def main():
     ap.add_argument("--march-steps", type=int, default=0, help="C4: time steps per simulation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C4 streaming entry")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
 
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and "WORLD_SIZE" in os.environ:
+    if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
-    if "WORLD_SIZE" not in os.environ:
-        world = 1
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -235,102 +234,117 @@ def main():
     ts = w.t_samples if w.n_steps == 0 else None
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
-
-    def step():
-        ctx.run_batch(n0_dev, w.c0, ts, w.target, stream=stream)
-        if world > 1:
-            out = ctx.moments(on_device=True)
-            grad = ctx.tangents(on_device=True, out=dict(grad=torch.empty((w.n_sims, P), dtype=torch.float64,
-                                                                          device=dev)))["grad"] if P else None
-            rec = D.pack_records(out["status"], out["steps"], out["moments"], out["loss"], grad)
-            D.allgather_records(rec, wg.n_sims)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
 
-    # ---- warm-up ----------------------------------------------------------------------------
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    res = ctx.moments()
-    steps_local = int(np.sum(res["steps"]))
-    assert np.all(res["status"] == 0), f"simulation failures: {np.unique(res['status'])}"
-    bu_local = float(w.N) * steps_local
+    def measure(ctx, w, n0_dev, ts, gather, clocks=None):
+        """W warm-up + K timed steps (CUDA events per step on the launch stream, L2 flushed
+        in between).  Returns (ms per step, max over ranks; this rank's bin-updates per
+        step; mean main-kernel ms measured by libpbe's events on the same stream)."""
+        P = w.n_tangents
 
-    # ---- timed region -------------------------------------------------------------------------
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        def step():
+            ctx.run_batch(n0_dev, w.c0, ts, w.target, stream=stream)
+            if gather and world > 1:
+                out = ctx.moments(on_device=True)
+                grad = (ctx.tangents(on_device=True, out=dict(grad=torch.empty((w.n_sims, P), dtype=torch.float64,
+                                                                               device=dev)))["grad"] if P else None)
+                rec = D.pack_records(out["status"], out["steps"], out["moments"], out["loss"], grad)
+                D.allgather_records(rec, wg.n_sims)
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        res = ctx.moments()
+        assert np.all(res["status"] == 0), f"simulation failures: {np.unique(res['status'])}"
+        bu = float(w.N) * float(np.sum(res["steps"]))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize(dev)
+        if clocks:
+            clocks.start()
+        kms = []
+        for k in range(args.steps):
+            flush.fill_(float(k))                              # evict L2 between timed iterations
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            if world == 1:
+                torch.cuda.synchronize(dev)
+                kms.append(ctx.last_run_info()["main_ms"])
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+        if not kms:
+            ctx.moments()
+            kms = [ctx.last_run_info()["main_ms"]]
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t[0])
+        return ms, bu, float(np.mean(kms))
+
+    def roofline(w, info, bu_local, kms, workload):
+        P = w.n_tangents
+        if info["kernel"] == pb.KERNEL_STREAM:
+            bytes_per = 16.0 * (1 + P)
+            achieved = bytes_per * bu_local / (kms * 1e-3) / 1e9
+            hbm = float(peaks.get("hbm_gbs", 6650.0))
+            r = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm, traffic=None,
+                     kernel="k_stream", bytes_per_bin_update=bytes_per,
+                     peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s", kernel_ms=kms)
+        else:
+            f = flops_per_bin_update(w.limiter, P)
+            achieved = f * bu_local / (kms * 1e-3) / 1e12
+            sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+            peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12     # FP64 FMA lanes x SMs x 2 flops x max SM clock
+            r = dict(bound="alu", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak, traffic=None,
+                     kernel="k_cluster" if info["kernel"] == pb.KERNEL_CLUSTER else "k_resident",
+                     flops_per_bin_update=f,
+                     peak_source=f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {sm_max:.0f} MHz", kernel_ms=kms)
+        # DRAM bytes of the kernel from an ncu --set full capture (profiles/traffic.json), as
+        # bytes per bin-update, scaled to this launch
+        prof = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(prof):
+            try:
+                tr = json.load(open(prof)).get(r["kernel"])
+                if tr is not None:
+                    r["traffic"] = tr["dram_bytes_per_bin_update"] * bu_local
+                    r["traffic_source"] = tr["source"]
+            except Exception:
+                pass
+        return r
+
+    # ---- main measurement ----------------------------------------------------------------------------
     clocks = ClockSampler(local_rank)
-    barrier()
-    torch.cuda.synchronize(dev)
-    clocks.start()
-    kernel_ms = []
-    for k in range(args.steps):
-        flush.fill_(float(k))                                  # evict L2 between timed iterations
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-        if world == 1:
-            torch.cuda.synchronize(dev)
-            kernel_ms.append(ctx.last_run_info()["main_ms"])
-    torch.cuda.synchronize(dev)
-    barrier()
+    ms, bu_local, kms = measure(ctx, w, n0_dev, ts, gather=True, clocks=clocks)
     clk = clocks.stop()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms, bu_local], dtype=torch.float64, device=dev)
-        mx = t.clone(); dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        sm = t.clone(); dist.all_reduce(sm[1:], op=dist.ReduceOp.SUM)
-        ms, bu_total = float(mx[0]), float(sm[1])
+        t = torch.tensor([bu_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        bu_total = float(t[0])
     else:
         bu_total = bu_local
     info = ctx.last_run_info()
     value = bu_total / (ms * 1e-3)
-
-    # ---- roofline of the dominant kernel ----------------------------------------------------------
-    if not kernel_ms:
-        ctx.run_batch(n0_dev, w.c0, ts, w.target, stream=stream)
-        ctx.moments()
-        kernel_ms = [ctx.last_run_info()["main_ms"]]
-    kms = float(np.mean(kernel_ms))
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    mb = None
+    roof = roofline(w, info, bu_local, kms, args.workload)
     try:
         import ctypes as C
         mbl = C.CDLL(os.path.join(ROOT, "paper_2411_00742_b200", "libpbe_mb.so"))
         mbl.pbe_mb_dfma_tflops.restype = C.c_double
-        mb = float(mbl.pbe_mb_dfma_tflops(local_rank, 5))
+        roof["dfma_microbench_tflops"] = float(mbl.pbe_mb_dfma_tflops(local_rank, 5))
     except Exception:
-        mb = None
-    if info["kernel"] == pb.KERNEL_STREAM:
-        bytes_per = 16.0 * (1 + P)
-        achieved = bytes_per * bu_local / (kms * 1e-3) / 1e9
-        hbm = float(peaks.get("hbm_gbs", 6650.0))
-        roof = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm, traffic=None,
-                    kernel="k_stream", peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s")
-    else:
-        f = flops_per_bin_update(w.limiter, P)
-        achieved = f * bu_local / (kms * 1e-3) / 1e12
-        peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12     # FP64 FMA lanes x SMs x 2 flops x max SM clock
-        roof = dict(bound="alu", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak, traffic=None,
-                    kernel="k_resident", flops_per_bin_update=f,
-                    peak_source=f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {sm_max:.0f} MHz",
-                    dfma_microbench_tflops=mb, kernel_ms=kms)
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            tr = json.load(open(prof)).get(args.workload)
-            if tr:
-                roof["traffic"] = tr
-        except Exception:
-            pass
+        pass
 
     # ---- e2e through the C ABI with pinned host buffers ------------------------------------------
     e2e = None
@@ -371,6 +385,20 @@ def main():
         e2e = dict(value=bu_total / (ms2 * 1e-3), unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
                    ms_per_step=ms2, host_buffers="pinned", api="C ABI pbe_run_batch(n0_on_device=0) + pbe_moments")
 
+    # ---- secondary (1 GPU): the C4 10^6-bin batch through the HBM-streaming kernel ----------------
+    secondary = None
+    if world == 1 and args.workload == "c5" and not args.no_secondary:
+        w4 = W.c4_sweep(1_000_000, batch=64, n_steps=1000)
+        ctx4 = pb.context_for(w4, device=local_rank)
+        n04 = torch.from_numpy(np.ascontiguousarray(w4.n0)).to(dev)
+        ms4, bu4, kms4 = measure(ctx4, w4, n04, None, gather=False)
+        info4 = ctx4.last_run_info()
+        secondary = dict(workload="C4 bin sweep N=1e6, batch 64, 1000 uncapped CFL steps", value=bu4 / (ms4 * 1e-3),
+                         unit=UNIT, ms_per_step=ms4, roofline=roofline(w4, info4, bu4, kms4, "c4"), kernel=info4,
+                         gpu_launches=int(info4["launches"]) * args.steps)
+        ctx4.close()
+        del n04
+
     # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -380,13 +408,14 @@ def main():
 
     if rank == 0:
         cfg = dict(desc)
-        cfg.update(parallelism=f"sims sharded round-robin over {world} GPU(s); NCCL allgather of per-sim records"
-                   if world > 1 else "1 GPU", l2="flushed between timed iterations (512 MiB write)",
-                   steps_per_sim_mean=steps_local / max(w.n_sims, 1), kernel=info)
+        cfg.update(parallelism=(f"sims sharded round-robin over {world} GPUs; NCCL allgather of per-sim records"
+                                if world > 1 else "1 GPU"), l2="flushed between timed iterations (512 MiB write)",
+                   steps_per_sim_mean=bu_local / w.N / max(w.n_sims, 1), kernel=info)
         line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
                     ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
                     data="synthetic (seeded; DESIGN.md input recipe)", config=cfg, roofline=roof,
-                    cpu_baseline=cpu, e2e=e2e, gpu_launches=int(info["launches"]) * args.steps, clocks=clk)
+                    cpu_baseline=cpu, e2e=e2e, gpu_launches=int(info["launches"]) * args.steps, clocks=clk,
+                    secondary=secondary)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -40,10 +40,10 @@ namespace pbe {
 // Smem halo: s_halo[(side * V + v) * HS + t + 1], HS = NT + 2, side 0/1 = bins 0/1 of
 // thread t, side 2/3 = bins K-2/K-1 (transposed so a warp's accesses are consecutive).
 // Columns 0 and NT + 1 stay zero: the ghost cells n_{-2} = n_{-1} = n_N = n_{N+1} = 0.
-template <int P, int K, bool NEG>
+template <int P, int K, bool NEG, class CdT>
 __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* __restrict__ s_halo,
                                            int NT, int tid, double C, double kap, double beta,
-                                           const double (&Cd)[P > 0 ? P : 1], bool vl, int i0, int N,
+                                           const CdT& Cd, bool vl, int i0, int N,
                                            double clip_thr) {
     constexpr int V = 1 + P;
     bool bad = false;
@@ -156,8 +156,8 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 // the neighbour's ghost column through distributed shared memory, every CTA pre-reduces
 // its warps' moment partials, and the scalar phase sums the CS CTA totals over DSMEM in
 // rank order.  The one barrier per step becomes a cluster barrier.
-template <int P, int K, int MAXT, bool CL = false>
-__global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
+template <int P, int K, int MAXT, bool CL = false, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     namespace cg = cooperative_groups;
     constexpr int V = 1 + P;
     constexpr int PP = P > 0 ? P : 1;
@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     __shared__ long long s_bad[2];              // step index that produced a negative
     __shared__ double s_nscale;
     __shared__ double s_cta[2][4][V];           // cluster mode: this CTA's moment totals
+    __shared__ double s_cdw[MINB > 1 ? 32 * PP : 1];   // per-warp Cdot slots (MINB = 2 variants)
 
     double x[V][K];
     // ---- load n0 (tangents start at 0: n0 does not depend on theta, R-20) --------------
@@ -374,14 +375,23 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const KParams kp) {
     long long n = 0;
     while (go) {
         const int q = (int)(n & 1), qp = q ^ 1;
-        double Cd[PP];
-#pragma unroll
-        for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? __shfl_sync(0xffffffffu, Cd_l, p) : 0.0;
-
         bool bad;
         const double* hin = s_halo + qp * HP;
-        if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
-        else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+        if (MINB == 1) {
+            // lane tangents of C in registers
+            double Cd[PP];
+#pragma unroll
+            for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? __shfl_sync(0xffffffffu, Cd_l, p) : 0.0;
+            if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+            else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+        } else {
+            // 2 CTAs/SM (<= 128 registers): lane tangents of C re-read from this warp's smem slot
+            volatile double* cdw = s_cdw + warp * PP;
+            if (lane < PP) cdw[lane] = Cd_l;
+            __syncwarp();
+            if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+            else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+        }
         if (bad) s_bad[q] = n;
         moment_partials(q, std::integral_constant<int, 3>{});     // mu3 of n and every tangent lane
         if (sample) {

@@ -65,6 +65,7 @@ struct pbe_ctx_s {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     pbe_run_info info{};
     int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
+    bool cluster2 = false;   // env PBE_CLUSTER2: 2-CTA clusters at 2 CTAs/SM for small N
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {
@@ -111,6 +112,13 @@ const ResidentVariant kResident[] = {
 
 // k_resident<P, K, MAXT, true> cluster variants (cluster size chosen at launch, <= 16)
 #define CV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T, true>}
+// 2 CTAs per SM (<= 128 registers/thread): a simulation split over a 2-CTA cluster keeps 16
+// warps per SM in two independent barrier domains (PBE_CLUSTER2=1 selects it for N <= 2048)
+const ResidentVariant kCluster2[] = {
+    ResidentVariant{8, 4, 256, &pbe::k_resident<8, 4, 256, true, 2>},
+    ResidentVariant{4, 4, 256, &pbe::k_resident<4, 4, 256, true, 2>},
+    ResidentVariant{0, 4, 256, &pbe::k_resident<0, 4, 256, true, 2>},
+};
 const ResidentVariant kCluster[] = {
     CV(0, 8, 512), CV(0, 16, 512),
     CV(2, 4, 512), CV(2, 8, 512),
@@ -288,6 +296,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     pbe_ctx ctx = new pbe_ctx_s();
     ctx->cfg = c;
     if (const char* e = getenv("PBE_LANES_PER_CTA")) ctx->group_max = atoi(e);
+    if (const char* e = getenv("PBE_CLUSTER2")) ctx->cluster2 = atoi(e) != 0;
     ctx->device = device;
     const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
     cudaError_t ea = cudaSuccess;
@@ -402,6 +411,11 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     const StreamVariant* sv = pick_stream(P);
     int cs = 1;
     const ResidentVariant* cv = pick_cluster(N, P, &cs);
+    if (ctx->cluster2 && cf.kernel == PBE_KERNEL_AUTO) {
+        const int Pi = P == 0 ? 0 : (P <= 4 ? 4 : (P <= 8 ? 8 : -1));
+        for (const auto& v : kCluster2)
+            if (v.P == Pi && v.K * v.maxt * 2 >= N) { cv = &v; cs = 2; rv = nullptr; break; }
+    }
     int kind = cf.kernel;
     if (kind == PBE_KERNEL_AUTO) kind = rv ? PBE_KERNEL_RESIDENT : (cv ? PBE_KERNEL_CLUSTER : PBE_KERNEL_STREAM);
     if (kind == PBE_KERNEL_CLUSTER && !cv)

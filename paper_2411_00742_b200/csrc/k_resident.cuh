@@ -326,10 +326,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     double C = 0.0, kap = 0.0, beta = 0.0, Cd_l = 0.0;
 
     // kinetics + time step of the next step from scalar state L (row a1, a2)
+    const KinCache KC = kin_cache(kp, KL, kT);
     auto kinetics = [&](LaneScal& L) -> bool {
-        const D1 T = temperature(kp, kT, L.t);
-        const D1 cs = solubility(kp, KL, T);
-        const D1 S = L.c / cs;
+        D1 T;
+        const D1 S = supersaturation(kp, KL, kT, KC, L.t, L.c, T);
         const D1 G = growth_rate(kp, KL, S, T);
         const double tn = steps_mode ? 0.0 : kp.t_samples[L.m];
         const StepScalars sc = time_step(kp, G, L.t, tn, steps_mode);
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         if (CL) {
             for (int r = 0; r < CS; ++r) a += cg::this_cluster().map_shared_rank(&s_cta[1][3][0], r)[0];
         } else {
-            for (int w = 0; w < NW; ++w) a += s_red[1][w][3][0];
+            a = sum4(&s_red[1][0][3][0], 4 * V, NW);
         }
         L.c = mk(kp.c0[s]); L.t = mk(0.0); L.mu3p = mk(a, 0.0); L.dt = mk(0.0);
         L.loss = 0.0; L.gacc = 0.0; L.rms_c = 1.0; L.rms_L = 1.0;
@@ -417,10 +417,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
                         if (pl >= 0) b += rc[1 + pl];
                     }
                 } else {
-                    for (int w = 0; w < NW; ++w) {
-                        a += s_red[q][w][km][0];
-                        if (pl >= 0) b += s_red[q][w][km][1 + pl];
-                    }
+                    a = sum4(&s_red[q][0][km][0], 4 * V, NW);
+                    if (pl >= 0) b = sum4(&s_red[q][0][km][1 + pl], 4 * V, NW);
                 }
                 tot[km] = a; totd[km] = b;
             }

@@ -239,9 +239,9 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl, kp.n_params, kp.n_params + kp.n_sol};
         const double* kT = kp.knot_T + (size_t)s * kp.knotT_stride;
         const D1 t = mk(W.t, T.t), c = mk(W.c, T.c);
-        const D1 Tk = temperature(kp, kT, t);
-        const D1 cs = solubility(kp, KL, Tk);
-        const D1 S = c / cs;
+        const KinCache KC = kin_cache(kp, KL, kT);
+        D1 Tk;
+        const D1 S = supersaturation(kp, KL, kT, KC, t, c, Tk);
         const D1 Gr = growth_rate(kp, KL, S, Tk);
         const double tn = steps_mode ? 0.0 : kp.t_samples[W.m];
         const StepScalars sc = time_step(kp, Gr, t, tn, steps_mode);

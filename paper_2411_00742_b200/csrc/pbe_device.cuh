@@ -148,12 +148,54 @@ __device__ __forceinline__ D1 growth_rate(const KParams& kp, const KinLoader& L,
         return mk(0.0);
     }
     if (S.v > 1.0) {                                                      // eq-poly_growth_rate
+        // sum_{j=1..k} a_j x^j in Horner form (short dependency chain on the step's critical
+        // path); parameters are loaded up front (independent of the chain)
         const D1 x = S - 1.0;
-        D1 g = mk(0.0), xp = x;
-        for (int j = 0; j < kp.n_params; ++j) { g = g + L.theta(j) * xp; xp = xp * x; }
-        return g;
+        D1 a[MAXTH];
+#pragma unroll
+        for (int j = 0; j < MAXTH; ++j) a[j] = (j < kp.n_params) ? L.theta(j) : mk(0.0);
+        D1 g = mk(0.0);
+#pragma unroll
+        for (int j = MAXTH - 1; j >= 0; --j)
+            if (j < kp.n_params) g = g * x + a[j];
+        return g * x;
     }
     return mk(0.0);
+}
+
+// Kinetics inputs that are constant when the temperature profile is constant (one knot):
+// T and 1/c*(T) are computed once, so a step needs no exp and no division for S.
+struct KinCache {
+    bool const_T;
+    D1 T, ics;
+};
+__device__ __forceinline__ KinCache kin_cache(const KParams& kp, const KinLoader& L, const double* kT) {
+    KinCache k;
+    k.const_T = (kp.n_knots == 1);
+    k.T = mk(kT[0]);
+    k.ics = k.const_T ? 1.0 / solubility(kp, L, k.T) : mk(0.0);
+    return k;
+}
+// S = c / c*(T(t)) (L285) and T
+__device__ __forceinline__ D1 supersaturation(const KParams& kp, const KinLoader& L, const double* kT,
+                                              const KinCache& kc, D1 t, D1 c, D1& T) {
+    if (kc.const_T) { T = kc.T; return c * kc.ics; }
+    T = temperature(kp, kT, t);
+    return c / solubility(kp, L, T);
+}
+
+// Fixed-order sum of n values base[0], base[stride], ... (n <= 32): four interleaved chains
+// then a pairwise combine — the same order everywhere (deterministic), shorter latency
+// than one sequential chain.
+__device__ __forceinline__ double sum4(const double* base, int stride, int n) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int w = 0; w < n; w += 4) {
+        a0 += base[(size_t)w * stride];
+        if (w + 1 < n) a1 += base[(size_t)(w + 1) * stride];
+        if (w + 2 < n) a2 += base[(size_t)(w + 2) * stride];
+        if (w + 3 < n) a3 += base[(size_t)(w + 3) * stride];
+    }
+    return (a0 + a1) + (a2 + a3);
 }
 
 // Per-step scalars produced by the kinetics warp and consumed by every thread.

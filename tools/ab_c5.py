@@ -20,7 +20,8 @@ for _ in range(3):
 bu = w.N * r['steps'].sum()
 print('RESULT', dict(ms=min(ms), rate=bu / (min(ms) * 1e-3), info=ctx.last_run_info(), ok=bool((r['status'] == 0).all())))
 """
-for env in ({}, {"PBE_CLUSTER2": "1"}):
+envs = [{}] if len(sys.argv) < 5 else [{}, dict(kv.split("=") for kv in sys.argv[4].split(","))]
+for env in envs:
     e = dict(os.environ, **env)
     out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

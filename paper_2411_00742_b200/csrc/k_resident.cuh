@@ -61,7 +61,15 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
     // Face between local bins (f-1, f).  For C >= 0: a = d_{f-1}, b = d_f, upwind f-1;
     // for C < 0: a = d_{f+1}, b = d_f, upwind f.  Primal parts first (shared by all lanes).
     double Fc = 0.0, Fdc[P > 0 ? P : 1];        // fluxes of the face shared with the previous bin
-    struct FaceP { double F, g, pak, pbk; };
+    // Face between local bins (f-1, f): primal flux F and the lane-flux coefficients.
+    //   C >= 0: a = d_{f-1}, b = d_f, upwind f-1;   C < 0: a = d_{f+1}, b = d_f, upwind f.
+    // Lane flux  Fdot = Cdot (n_up + beta psi) + C ndot_up + kap (pa adot + pb bdot)
+    // regrouped over the three cells it touches (lo = f-2 | f-1, mid, hi = f | f+1):
+    //   C >= 0: w_hi ndot_f + w_mid ndot_{f-1} + w_lo ndot_{f-2},
+    //           w_hi = kap pb, w_mid = C + kap (pa - pb), w_lo = -kap pa
+    //   C <  0: w_hi ndot_{f+1} + w_mid ndot_f + w_lo ndot_{f-1},
+    //           w_hi = kap pa, w_mid = C - kap (pa - pb), w_lo = -kap pb
+    struct FaceP { double F, g, w_lo, w_mid, w_hi; };
     auto face_primal = [&](int f) -> FaceP {
         const int u = NEG ? f : f - 1;
         const int ja = NEG ? f + 1 : f - 1;
@@ -72,15 +80,14 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
         FaceP r;
         r.F = fma(C, nup, kap2 * h);                   // C n_up + kap psi
         r.g = fma(beta2, h, nup);                      // n_up + beta psi
-        r.pak = kap2 * qa;                             // kap d psi/da
-        r.pbk = kap2 * qb;                             // kap d psi/db
+        const double pak = kap2 * qa, pbk = kap2 * qb; // kap d psi/da, kap d psi/db
+        if (!NEG) { r.w_hi = pbk; r.w_mid = C + (pak - pbk); r.w_lo = -pak; }
+        else      { r.w_hi = pak; r.w_mid = C - (pak - pbk); r.w_lo = -pbk; }
         return r;
     };
     auto face_lane = [&](int f, int p, const FaceP& fp) -> double {
-        const int u = NEG ? f : f - 1;
-        const int ja = NEG ? f + 1 : f - 1;
-        const double ad = X(1 + p, ja) - X(1 + p, ja - 1), bd = X(1 + p, f) - X(1 + p, f - 1);
-        return fma(Cd[p], fp.g, fma(C, X(1 + p, u), fma(fp.pak, ad, fp.pbk * bd)));
+        const int lo = NEG ? f - 1 : f - 2;
+        return fma(Cd[p], fp.g, fma(fp.w_hi, X(1 + p, lo + 2), fma(fp.w_mid, X(1 + p, lo + 1), fp.w_lo * X(1 + p, lo))));
     };
     // update bin k from its two faces; the lane fluxes of the far face come from Fdc and
     // are replaced in place by the near face's (so only one array of lane fluxes is live)

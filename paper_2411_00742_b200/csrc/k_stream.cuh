@@ -147,12 +147,15 @@ __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int R
         const double nup = x[0][u];
         F[f - 2] = fma(C, nup, kap2 * h);
         if (P > 0) {
+            // lane flux regrouped over the three cells it touches (see k_resident.cuh face_lane)
             const double gq = fma(beta2, h, nup), pak = kap2 * qa, pbk = kap2 * qb;
+            const int lo = NEG ? f - 1 : f - 2;
+            const double w_hi = NEG ? pak : pbk;
+            const double w_mid = NEG ? C - (pak - pbk) : C + (pak - pbk);
+            const double w_lo = NEG ? -pbk : -pak;
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const double ad = x[1 + p][ja] - x[1 + p][ja - 1], bd = x[1 + p][f] - x[1 + p][f - 1];
-                Fd[f - 2][p] = fma(cf.Cd[p], gq, fma(C, x[1 + p][u], fma(pak, ad, pbk * bd)));
-            }
+            for (int p = 0; p < P; ++p)
+                Fd[f - 2][p] = fma(cf.Cd[p], gq, fma(w_hi, x[1 + p][lo + 2], fma(w_mid, x[1 + p][lo + 1], w_lo * x[1 + p][lo])));
         }
     }
     double y[V][K];

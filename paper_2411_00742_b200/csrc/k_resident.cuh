@@ -92,8 +92,9 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
     // update bin k from its two faces; the lane fluxes of the far face come from Fdc and
     // are replaced in place by the near face's (so only one array of lane fluxes is live)
     bool neg = false;
-    auto step_bin = [&](int k, int f_new, bool new_is_left) {
-        const FaceP fp = face_primal(f_new);
+    // update bin k from its new face (primal part fp, computed one iteration ahead so its
+    // reciprocal chain overlaps the previous face's lane work) and the carried face fluxes
+    auto step_bin = [&](int k, int f_new, bool new_is_left, const FaceP& fp) {
         const double dF = new_is_left ? (Fc - fp.F) : (fp.F - Fc);
         const double nn = x[0][k] - dF;
         neg |= (nn < 0.0);
@@ -114,8 +115,13 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 #pragma unroll
             for (int p = 0; p < P; ++p) Fdc[p] = face_lane(K, p, fp);
         }
+        FaceP fp = face_primal(K - 1);
 #pragma unroll
-        for (int k = K - 1; k >= 0; --k) step_bin(k, k, true);        // left face of bin k: reads bins < k (old)
+        for (int k = K - 1; k >= 0; --k) {          // left face of bin k: reads bins < k (old)
+            const FaceP fnext = k > 0 ? face_primal(k - 1 > 0 ? k - 1 : 0) : fp;
+            step_bin(k, k, true, fp);
+            fp = fnext;
+        }
     } else {
         {   // left face of bin 0
             const FaceP fp = face_primal(0);
@@ -123,8 +129,13 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 #pragma unroll
             for (int p = 0; p < P; ++p) Fdc[p] = face_lane(0, p, fp);
         }
+        FaceP fp = face_primal(1);
 #pragma unroll
-        for (int k = 0; k < K; ++k) step_bin(k, k + 1, false);        // right face of bin k: reads bins > k (old)
+        for (int k = 0; k < K; ++k) {               // right face of bin k: reads bins > k (old)
+            const FaceP fnext = k + 1 < K ? face_primal(k + 2 < K + 1 ? k + 2 : K) : fp;
+            step_bin(k, k + 1, false, fp);
+            fp = fnext;
+        }
     }
     // Clip (R-17), applied after the sweep (every face above used OLD values, so deferring
     // it is exact): round-off negatives and ghost bins i >= N become exactly 0 together with

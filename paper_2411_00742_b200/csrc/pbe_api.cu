@@ -66,6 +66,7 @@ struct pbe_ctx_s {
     pbe_run_info info{};
     int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
     bool cluster2 = false;   // env PBE_CLUSTER2: 2-CTA clusters at 2 CTAs/SM for small N
+    int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {
@@ -169,8 +170,10 @@ int lanes_per_cta(int P, int group_max) {
     return 5;                      // 9..10 lanes: 2 groups of 5
 }
 
-// smallest K (most warps) whose CTA covers N bins
-const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups) {
+// Resident variant for N bins: one simulation alone wants the smallest K (most warps); a
+// batch wants small CTAs so several simulations share an SM and hide each other's per-step
+// latency (K_pref from PBE_RESIDENT_K or the heuristic in pbe_run_batch).
+const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups, int k_pref = 0) {
     const int Pi = lanes_per_cta(P, group_max);
     *groups = Pi ? (P + Pi - 1) / Pi : 1;
     const ResidentVariant* best = nullptr;
@@ -179,7 +182,11 @@ const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups) {
         if ((long long)v.K * v.maxt < N) continue;
         const int nt = ((N + v.K - 1) / v.K + 31) / 32 * 32;
         if (resident_smem(v, nt) > 200 * 1024) continue;      // + <= 20 KB static < 227 KB
-        if (!best || v.K < best->K) best = &v;
+        if (!best) { best = &v; continue; }
+        const bool closer = k_pref ? (abs(v.K - k_pref) < abs(best->K - k_pref) ||
+                                      (abs(v.K - k_pref) == abs(best->K - k_pref) && v.K < best->K))
+                                   : v.K < best->K;
+        if (closer) best = &v;
     }
     return best;
 }
@@ -297,6 +304,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     ctx->cfg = c;
     if (const char* e = getenv("PBE_LANES_PER_CTA")) ctx->group_max = atoi(e);
     if (const char* e = getenv("PBE_CLUSTER2")) ctx->cluster2 = atoi(e) != 0;
+    if (const char* e = getenv("PBE_RESIDENT_K")) ctx->resident_k = atoi(e);
     ctx->device = device;
     const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
     cudaError_t ea = cudaSuccess;
@@ -407,7 +415,8 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
 
     // kernel choice: register-resident when the simulation fits one CTA, else streaming
     int groups = 1;
-    const ResidentVariant* rv = pick_resident(N, P, ctx->group_max, &groups);
+    int k_pref = ctx->resident_k;
+    const ResidentVariant* rv = pick_resident(N, P, ctx->group_max, &groups, k_pref);
     const StreamVariant* sv = pick_stream(P);
     int cs = 1;
     const ResidentVariant* cv = pick_cluster(N, P, &cs);

@@ -103,7 +103,7 @@ size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * 
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {
-    RV(0, 2, 512), RV(0, 4, 512), RV(0, 8, 512), RV(0, 16, 512),
+    RV(0, 2, 512), RV(0, 4, 512), RV(0, 8, 512), RV(0, 16, 512), RV(0, 32, 256),
     RV(2, 2, 512), RV(2, 4, 512), RV(2, 8, 512), RV(2, 16, 256),
     RV(4, 2, 512), RV(4, 4, 512), RV(4, 8, 256),
     RV(5, 2, 512), RV(5, 4, 512), RV(5, 8, 256),
@@ -416,6 +416,9 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     // kernel choice: register-resident when the simulation fits one CTA, else streaming
     int groups = 1;
     int k_pref = ctx->resident_k;
+    // batches of >= 2 simulations per SM: fat threads, small CTAs (several per SM overlap
+    // their per-step latency); measured 4.4x at N = 1000
+    if (!k_pref && P == 0 && n_sims >= 2 * 148) k_pref = 16;
     const ResidentVariant* rv = pick_resident(N, P, ctx->group_max, &groups, k_pref);
     const StreamVariant* sv = pick_stream(P);
     int cs = 1;

@@ -44,6 +44,7 @@ class _Problem(C.Structure):
         ("knot_T", C.POINTER(C.c_double)), ("knot_T_stride", C.c_int64),
         ("M", C.c_int32), ("t_samples", C.POINTER(C.c_double)),
         ("n_tan", C.c_int32), ("tangent_seed", C.POINTER(C.c_double)),
+        ("N2", C.c_int32), ("L2_lo", C.c_double), ("dL2", C.c_double),
     ]
 
 
@@ -71,6 +72,10 @@ def _load():
         lib.oracle_sweep.argtypes = [C.c_int32, dp, C.c_double, C.c_int32, dp]
         lib.oracle_moments.argtypes = [C.POINTER(_Problem), dp, dp]
         lib.oracle_dual_si_example.argtypes = [C.c_double] * 4 + [dp]
+        lib.oracle_run_batch_2d.argtypes = [C.POINTER(_Problem), C.c_int32, dp, dp, C.c_int64, dp, dp, ip, lp, dp,
+                                            C.c_int32]
+        lib.oracle_run_batch_2d.restype = C.c_int
+        lib.oracle_split_step_2d.argtypes = [C.c_int32, C.c_int32, dp, C.c_double, C.c_double, C.c_int32, dp]
         _lib = lib
     return _lib
 
@@ -93,7 +98,8 @@ def _problem(w, keep):
         law=w.law, n_params=w.n_params, sol_kind=w.sol_kind, n_sol=int(sol.shape[0]), sol=_dp(sol),
         n_knots=int(kt.shape[0]), knot_t=_dp(kt), knot_T=_dp(kT),
         knot_T_stride=int(kt.shape[0]) if kT.shape[0] > 1 else 0,
-        M=int(ts.shape[0]), t_samples=_dp(ts), n_tan=w.n_tangents, tangent_seed=_dp(seed))
+        M=int(ts.shape[0]), t_samples=_dp(ts), n_tan=w.n_tangents, tangent_seed=_dp(seed),
+        N2=getattr(w, "N2", 0), L2_lo=getattr(w, "L2_lo", 0.0), dL2=getattr(w, "dL2", 0.0))
 
 
 def run(w, mode: int = MODE_DOUBLE, threads: int = 1, want_n: bool = True) -> dict:
@@ -180,3 +186,31 @@ def dual_si_example(x1: float, x2: float, v1: float, v2: float):
     out = np.zeros(4)
     lib.oracle_dual_si_example(x1, x2, v1, v2, _dp(out))
     return tuple(out)
+
+
+def run2d(w, threads: int = 1, want_f: bool = True) -> dict:
+    """NEXT-1 2D march (Godunov splitting) of every simulation of 2D workload `w`:
+    samples [S][M][8] = (t, c, mu00, mu10, mu01, mu11, mu02, mu12), status, steps,
+    f_final [S][N2][N1] (L1 fastest)."""
+    lib = _load()
+    keep = []
+    pb = _problem(w, keep)
+    S, M, NN = w.n_sims, w.M, w.N * w.N2
+    theta = _f64(w.theta); f0 = _f64(w.n0); c0 = _f64(w.c0)
+    samples = np.full((S, M, 8), np.nan)
+    status = np.zeros(S, np.int32); steps = np.zeros(S, np.int64)
+    f_final = np.zeros((S, w.N2, w.N)) if want_f else None
+    rc = lib.oracle_run_batch_2d(C.byref(pb), S, _dp(theta), _dp(f0), NN if f0.shape[0] > 1 else 0, _dp(c0),
+                                 _dp(samples), status.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 steps.ctypes.data_as(C.POINTER(C.c_int64)), _dp(f_final), threads)
+    if rc != 0:
+        raise RuntimeError(f"oracle_run_batch_2d failed ({rc})")
+    return dict(samples=samples, status=status, steps=steps, f_final=f_final)
+
+
+def split_step_2d(f, C1: float, C2: float, limiter: int) -> np.ndarray:
+    """One Godunov-split step (rows along L1 with C1, then columns along L2 with C2) of f[N2][N1]."""
+    lib = _load()
+    f = _f64(f); out = np.zeros_like(f)
+    lib.oracle_split_step_2d(int(f.shape[1]), int(f.shape[0]), _dp(f), float(C1), float(C2), int(limiter), _dp(out))
+    return out

@@ -132,6 +132,10 @@ typedef struct {
     const double* t_samples;  // [M] strictly increasing, > 0
     int32_t n_tan;            // tangent lanes (0..10)
     const double* tangent_seed;  // [n_tan][n_params + n_sol]; NULL => unit vectors over theta
+    // 2D model (NEXT-1): N2 > 0 adds the second length L2 (bins j, centers L2_lo + (j+1/2) dL2);
+    // theta = [dimension-1 law | dimension-2 law] (n_params even)
+    int32_t N2;
+    double L2_lo, dL2;
 } oracle_problem;
 }
 
@@ -510,4 +514,165 @@ void oracle_dual_si_example(double x1, double x2, double v1, double v2, double* 
     out[0] = y1.v; out[1] = y2.v; out[2] = y1.d[0]; out[3] = y2.d[0];
 }
 
+}  // extern "C"
+
+// =====================================================================================
+//  NEXT-1: the paper's 2D model (eq-PBE_batch_2d, L257-266) with Godunov dimensional
+//  splitting (L291: "update the PSSD ... along each spatial dimension separately (i.e.
+//  twice)"): every row along L1 with C1 = G1 dt / dL1, then every column along L2 with
+//  C2 = G2 dt / dL2, each with eq-highRes_growth.  dt = nu min(dL1/|G1|, dL2/|G2|) (SI L859),
+//  mass balance with mu_12 = sum dL1 dL2 L1 L2^2 f (eq-discrete_mass_balance, L304-312).
+//  Records (t, c, mu00, mu10, mu01, mu11, mu02, mu12) (SPEC MomentVector).  double only.
+// =====================================================================================
+namespace oracle {
+
+struct Rec2D { double t, c, mu[6]; };
+
+inline void moments2d(const oracle_problem& pb, const std::vector<double>& f, double mu[6]) {
+    // (p, q) = (0,0) (1,0) (0,1) (1,1) (0,2) (1,2)  (SI eq-moment2D, L873)
+    static const int PQ[6][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}, {0, 2}, {1, 2}};
+    const int N1 = pb.N, N2 = pb.N2;
+    for (int k = 0; k < 6; ++k) {
+        Neumaier acc;
+        for (int j = 0; j < N2; ++j) {
+            const double L2 = pb.L2_lo + ((double)j + 0.5) * pb.dL2;
+            for (int i = 0; i < N1; ++i) {
+                const double L1 = pb.L_lo + ((double)i + 0.5) * pb.dL;
+                acc.add(pb.dL * pb.dL2 * std::pow(L1, (double)PQ[k][0]) * std::pow(L2, (double)PQ[k][1]) *
+                        f[(size_t)j * N1 + i]);
+            }
+        }
+        mu[k] = acc.get();
+    }
+}
+
+inline int simulate2d(const oracle_problem& pb, const double* theta, const double* f0, double c0,
+                      std::vector<Rec2D>& rec, std::vector<double>& f, int64_t& steps) {
+    const int N1 = pb.N, N2 = pb.N2, H = pb.n_params / 2;
+    oracle_problem p1 = pb;
+    p1.n_params = H;
+    std::vector<double> sol(pb.sol, pb.sol + pb.n_sol);
+    f.assign(f0, f0 + (size_t)N1 * N2);
+    double nscale = 0.0;
+    for (double v : f) nscale = std::max(nscale, v);
+    double c = c0, t = 0.0, mu[6];
+    moments2d(pb, f, mu);
+    double mu12p = mu[5];
+    int m = 0;
+    steps = 0;
+    rec.assign(pb.n_steps > 0 ? 1 : pb.M, Rec2D{NAN, NAN, {NAN, NAN, NAN, NAN, NAN, NAN}});
+    std::vector<double> line, out;
+    while (true) {
+        if (pb.n_steps > 0) { if (steps >= pb.n_steps) break; }
+        else if (m >= pb.M) break;
+        if (steps >= pb.max_steps) return ST_MAXSTEPS;
+        const double T = temperature<double>(pb, t);
+        const double cs = solubility<double>(pb, sol.data(), T);
+        const double S = c / cs;
+        const double G1 = growth_rate<double>(p1, theta, S, T);
+        const double G2 = growth_rate<double>(p1, theta + H, S, T);
+        // SI L859: dt = nu min(dL1/|G1|, dL2/|G2|) (a zero rate does not limit), capped (R-7, R-8)
+        double dt = pb.dt_max;
+        if (pb.dt_fixed > 0.0) dt = pb.dt_fixed;
+        else {
+            double dtc = INFINITY;
+            if (G1 != 0.0) dtc = std::min(dtc, pb.courant * pb.dL / std::fabs(G1));
+            if (G2 != 0.0) dtc = std::min(dtc, pb.courant * pb.dL2 / std::fabs(G2));
+            dt = std::min(dtc, pb.dt_max);
+        }
+        bool landing = false;
+        if (pb.n_steps <= 0) {
+            const double tn = pb.t_samples[m];
+            if (t + dt >= tn - 1e-9 * dt) { dt = tn - t; landing = true; }   // land on the sample (R-8)
+        } else if (std::isinf(dt)) {
+            dt = 0.0;
+        }
+        const double C1 = G1 * dt / pb.dL, C2 = G2 * dt / pb.dL2;
+        if (std::fabs(C1) > 1.0 || std::fabs(C2) > 1.0) return ST_CFL;
+        // sweep 1: every row along L1
+        std::vector<double> g(f.size());
+        line.resize(N1); out.resize(N1);
+        for (int j = 0; j < N2; ++j) {
+            for (int i = 0; i < N1; ++i) line[i] = f[(size_t)j * N1 + i];
+            sweep<double>(line, C1, pb.limiter, out);
+            for (int i = 0; i < N1; ++i) g[(size_t)j * N1 + i] = out[i];
+        }
+        // sweep 2: every column along L2, on the result of sweep 1
+        line.resize(N2); out.resize(N2);
+        for (int i = 0; i < N1; ++i) {
+            for (int j = 0; j < N2; ++j) line[j] = g[(size_t)j * N1 + i];
+            sweep<double>(line, C2, pb.limiter, out);
+            for (int j = 0; j < N2; ++j) g[(size_t)j * N1 + i] = out[j];
+        }
+        bool bad = false;
+        for (double& v : g)
+            if (v < 0.0) { if (v >= -1e-12 * nscale) v = 0.0; else bad = true; }
+        if (bad) return ST_NEGATIVE;
+        double mun[6];
+        moments2d(pb, g, mun);
+        const double cn = c - pb.rho_c * pb.k_v * (mun[5] - mu12p);
+        if (cn < 0.0) return ST_INFEASIBLE;
+        f.swap(g);
+        c = cn;
+        mu12p = mun[5];
+        for (int k = 0; k < 6; ++k) mu[k] = mun[k];
+        t = landing ? pb.t_samples[m] : t + dt;
+        ++steps;
+        if (landing) { rec[m] = Rec2D{t, c, {mu[0], mu[1], mu[2], mu[3], mu[4], mu[5]}}; ++m; }
+    }
+    if (pb.n_steps > 0) rec[0] = Rec2D{t, c, {mu[0], mu[1], mu[2], mu[3], mu[4], mu[5]}};
+    return ST_OK;
+}
+
+}  // namespace oracle
+
+extern "C" {
+// 2D march of n_sims simulations: samples [S][M][8], f_final [S][N2][N1] (nullable).
+int oracle_run_batch_2d(const oracle_problem* pb, int32_t n_sims, const double* theta, const double* f0,
+                        int64_t f0_stride, const double* c0, double* samples, int32_t* status, int64_t* steps,
+                        double* f_final, int32_t n_threads) {
+    if (!pb || pb->N2 < 1 || (pb->n_params % 2) != 0) return 1;
+    const int Mr = pb->n_steps > 0 ? 1 : pb->M;
+    std::atomic<int> next{0};
+    auto work = [&]() {
+        for (int s = next++; s < n_sims; s = next++) {
+            oracle_problem pbs = *pb;
+            pbs.knot_T = pb->knot_T + (size_t)s * pb->knot_T_stride;
+            std::vector<oracle::Rec2D> rec;
+            std::vector<double> f;
+            int64_t st = 0;
+            status[s] = oracle::simulate2d(pbs, theta + (size_t)s * pb->n_params, f0 + (size_t)s * f0_stride, c0[s],
+                                           rec, f, st);
+            steps[s] = st;
+            for (int m = 0; m < Mr; ++m) {
+                double* o = samples + ((size_t)s * Mr + m) * 8;
+                o[0] = rec[m].t; o[1] = rec[m].c;
+                for (int k = 0; k < 6; ++k) o[2 + k] = rec[m].mu[k];
+            }
+            if (f_final) std::copy(f.begin(), f.end(), f_final + (size_t)s * pb->N * pb->N2);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 0; w < std::max(1, (int)n_threads); ++w) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+    return 0;
+}
+
+// one Godunov-split step of a 2D field (probe): rows along L1 with C1, then columns with C2
+void oracle_split_step_2d(int32_t N1, int32_t N2, const double* f, double C1, double C2, int32_t limiter, double* out) {
+    std::vector<double> g(f, f + (size_t)N1 * N2), line, o;
+    line.resize(N1); o.resize(N1);
+    for (int j = 0; j < N2; ++j) {
+        for (int i = 0; i < N1; ++i) line[i] = g[(size_t)j * N1 + i];
+        oracle::sweep<double>(line, C1, limiter, o);
+        for (int i = 0; i < N1; ++i) g[(size_t)j * N1 + i] = o[i];
+    }
+    line.resize(N2); o.resize(N2);
+    for (int i = 0; i < N1; ++i) {
+        for (int j = 0; j < N2; ++j) line[j] = g[(size_t)j * N1 + i];
+        oracle::sweep<double>(line, C2, limiter, o);
+        for (int j = 0; j < N2; ++j) g[(size_t)j * N1 + i] = o[j];
+    }
+    std::copy(g.begin(), g.end(), out);
+}
 }  // extern "C"

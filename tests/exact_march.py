@@ -155,3 +155,42 @@ def march(num, *, N, dL, L_lo, limiter, courant, dt_fixed, dt_max, law, theta, s
     if n_steps:
         recs.append((t, c, *mom(n)))
     return recs, n, steps
+
+
+def march_2d(num, *, N1, N2, dL1, dL2, limiter, dt_fixed, law, theta, sol_kind, sol, T, f0, c0, rho_c, k_v,
+             t_samples):
+    """Exact 2D Godunov-split march (rows along L1, then columns along L2, flux form) with
+    fixed dt landing on the sample times; returns records (t, c, mu00, mu10, mu01, mu11,
+    mu02, mu12) and the final field [N2][N1]."""
+    f = [[num(f0[j * N1 + i]) for i in range(N1)] for j in range(N2)]
+    c, t = num(c0), num(0)
+    L1 = [(num(i) + num("0.5")) * num(dL1) for i in range(N1)]
+    L2 = [(num(j) + num("0.5")) * num(dL2) for j in range(N2)]
+    w = num(dL1) * num(dL2)
+    PQ = [(0, 0), (1, 0), (0, 1), (1, 1), (0, 2), (1, 2)]
+    mom = lambda g: [sum(w * L1[i] ** p * L2[j] ** q * g[j][i] for j in range(N2) for i in range(N1)) for p, q in PQ]
+    H = len(theta) // 2
+    mu12 = mom(f)[5]
+    recs, m = [], 0
+    Tn = num(T)
+    while m < len(t_samples):
+        S = c / solubility(num, sol_kind, sol, Tn)
+        G1 = growth(num, law, theta[:H], S, Tn)
+        G2 = growth(num, law, theta[H:], S, Tn)
+        dt = num(dt_fixed)
+        tn = num(t_samples[m])
+        landing = t + dt >= tn - num("1e-9") * dt
+        if landing:
+            dt = tn - t
+        C1, C2 = G1 * dt / num(dL1), G2 * dt / num(dL2)
+        f = [flux_step(row, C1, limiter) for row in f]
+        cols = [flux_step([f[j][i] for j in range(N2)], C2, limiter) for i in range(N1)]
+        f = [[cols[i][j] for i in range(N1)] for j in range(N2)]
+        mu = mom(f)
+        c = c - num(rho_c) * num(k_v) * (mu[5] - mu12)
+        mu12 = mu[5]
+        t = tn if landing else t + dt
+        if landing:
+            recs.append((t, c, *mu))
+            m += 1
+    return recs, f

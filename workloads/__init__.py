@@ -75,6 +75,10 @@ class Workload:
     n_tangents: int = 0
     tangent_seed: Optional[np.ndarray] = None  # [n_tangents][P + n_sol]
     meta: dict = field(default_factory=dict)
+    # 2D model (NEXT-1): N2 > 0 -> n0 rows hold N2 * N1 values (L1 fastest); theta = [dim 1 | dim 2]
+    N2: int = 0
+    dL2: float = 0.0
+    L2_lo: float = 0.0
 
     @property
     def n_sims(self) -> int:
@@ -220,3 +224,35 @@ CONFIGS = {
     "c4": c4_sweep,
     "c5": c5_ensemble,
 }
+
+
+# Table A.1 (L722-727): growth-rate constants for the two crystal dimensions (growth only)
+ARRHENIUS_2D = (8.86e6, 2.45e3, 3.7, 4.088e5, 2.4e3, 2.5)
+
+
+def gaussian_seed_2d(N1: int, dL1: float, N2: int, dL2: float, mean=(400.0, 250.0), sigma=(30.0, 30.0),
+                     m0: float = 1.0, rho_c: float = RHO_C, k_v: float = K_V) -> np.ndarray:
+    """Bivariate normal seed with independent marginals (Table 1) at cell centers,
+    scaled analytically to crystal mass rho_c k_v E[L1 L2^2] N_c = m0 (SI S1.3, L887);
+    returns [N2][N1] flattened (L1 fastest)."""
+    L1 = bin_centers(N1, dL1)
+    L2 = bin_centers(N2, dL2)
+    Nc = m0 / (rho_c * k_v * mean[0] * (mean[1] ** 2 + sigma[1] ** 2))
+    g1 = np.exp(-0.5 * ((L1 - mean[0]) / sigma[0]) ** 2) / (sigma[0] * math.sqrt(2 * math.pi))
+    g2 = np.exp(-0.5 * ((L2 - mean[1]) / sigma[1]) ** 2) / (sigma[1] * math.sqrt(2 * math.pi))
+    return (Nc * np.outer(g2, g1)).reshape(-1)
+
+
+def c2d_base(N1: int = 1200, N2: int = 600, t_max: float = 10.0, M: int = 10, n_sims: int = 1,
+             dt_max: float = math.inf, limiter: int = LIM_VANLEER) -> Workload:
+    """NEXT-1 / Table 1 base case: 2D PSSD on L1 in [0, 1200] x L2 in [0, 600] um, Gaussian seed
+    (400, 250) um, sigma 30 um, m0 = 1 g/kg, c0 = 8 g/kg, T = 15 C, Arrhenius growth for both
+    dimensions (Table A.1), CFL nu = 0.9 over both dimensions (SI L859)."""
+    dL1, dL2 = 1200.0 / N1, 600.0 / N2
+    return Workload(
+        name=f"c2d_base_{N1}x{N2}", N=N1, dL=dL1, N2=N2, dL2=dL2, limiter=limiter, dt_max=dt_max,
+        law=LAW_ARRHENIUS, theta=np.tile(np.array(ARRHENIUS_2D), (n_sims, 1)),
+        sol_kind=SOL_EXP, sol=np.array(SOL_EXP_DEFAULT),
+        knot_t=np.array([0.0]), knot_T=np.array([[15.0]]),
+        n0=gaussian_seed_2d(N1, dL1, N2, dL2)[None, :], c0=np.full(n_sims, 8.0),
+        t_samples=np.linspace(t_max / M, t_max, M))

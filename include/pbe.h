@@ -70,7 +70,8 @@ enum {
     PBE_KERNEL_AUTO = 0,      /* choose by N and lanes              */
     PBE_KERNEL_RESIDENT = 1,  /* one CTA per sim, state in registers across all steps     */
     PBE_KERNEL_CLUSTER = 2,   /* thread-block cluster per sim, DSMEM halo + reduction     */
-    PBE_KERNEL_STREAM = 3     /* grid-wide persistent kernel, HBM streaming, grid barrier */
+    PBE_KERNEL_STREAM = 3,    /* grid-wide persistent kernel, HBM streaming, grid barrier */
+    PBE_KERNEL_2D = 4         /* 2D model (set by n_bins2 > 0): grid-wide split-sweep kernel */
 };
 
 typedef struct {
@@ -90,6 +91,17 @@ typedef struct {
     int32_t n_tangents;  /* 0..10 forward-mode tangent lanes */
     int32_t max_sims;    /* capacity (>= n_sims of every later call) */
     int32_t kernel;      /* PBE_KERNEL_* (AUTO unless forcing a variant) */
+    /* --- 2D model (NEXT-1; eq-PBE_batch_2d L257-266, Godunov splitting L291) ----------
+     * n_bins2 > 0 selects the paper's 2D model: f(L1, L2) on n_bins x n_bins2 cells, L2 bin j
+     * centered at L2_lo + (j + 1/2) dL2; each step sweeps every row along L1 then every
+     * column along L2 (eq-highRes_growth), dt = nu min(dL1/|G1|, dL2/|G2|) (SI L859), mass
+     * balance on mu_12 = sum dL1 dL2 L1 L2^2 f (L271, L304-312).  In 2D mode: kinetics theta
+     * = [dimension-1 law | dimension-2 law] (n_params even), n_tangents must be 0, n0 /
+     * n_final are [sims][n_bins2][n_bins] (L1 fastest), and pbe_moments records are
+     * [sims][M][8] = (t, c, mu00, mu10, mu01, mu11, mu02, mu12).  0 = 1D. */
+    int32_t n_bins2;
+    double  L2_lo;
+    double  dL2;
 } pbe_config;
 
 /* Creates a context on CUDA device `device` and allocates its device scratch for

@@ -26,7 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIM_UPWIND, LIM_VANLEER = 0, 1
 LAW_CONST, LAW_ARRHENIUS_GD, LAW_POLY = 0, 1, 2
 SOL_EXP, SOL_POLY = 0, 1
-KERNEL_AUTO, KERNEL_RESIDENT, KERNEL_CLUSTER, KERNEL_STREAM = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_RESIDENT, KERNEL_CLUSTER, KERNEL_STREAM, KERNEL_2D = 0, 1, 2, 3, 4
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_CFL", 3: "ERR_NEGATIVE", 4: "ERR_INFEASIBLE",
           5: "ERR_MAXSTEPS", 6: "ERR_CUDA", 7: "ERR_NOMEM", 8: "ERR_STATE"}
 
@@ -46,7 +46,7 @@ class _Config(C.Structure):
                 ("courant", C.c_double), ("dt_fixed", C.c_double), ("dt_max", C.c_double),
                 ("max_steps", C.c_int64), ("n_steps", C.c_int64), ("rho_c", C.c_double), ("k_v", C.c_double),
                 ("n_samples", C.c_int32), ("n_tangents", C.c_int32), ("max_sims", C.c_int32),
-                ("kernel", C.c_int32)]
+                ("kernel", C.c_int32), ("n_bins2", C.c_int32), ("L2_lo", C.c_double), ("dL2", C.c_double)]
 
 
 class RunInfo(C.Structure):
@@ -118,10 +118,11 @@ class Context:
                  courant: float = 0.9, dt_fixed: float = 0.0, dt_max: float = math.inf,
                  max_steps: int = 10_000_000, n_steps: int = 0, rho_c: float = 1.11e-12,
                  k_v: float = math.pi / 4, n_samples: int = 1, n_tangents: int = 0, max_sims: int = 1,
-                 kernel: int = KERNEL_AUTO, device: int = 0):
+                 kernel: int = KERNEL_AUTO, device: int = 0, n_bins2: int = 0, L2_lo: float = 0.0,
+                 dL2: float = 0.0):
         self._lib = load_library()
         self.cfg = _Config(n_bins, L_lo, dL, limiter, courant, dt_fixed, dt_max, max_steps, n_steps, rho_c,
-                           k_v, n_samples, n_tangents, max_sims, kernel)
+                           k_v, n_samples, n_tangents, max_sims, kernel, n_bins2, L2_lo, dL2)
         h = C.c_void_p()
         st = self._lib.pbe_create(C.byref(self.cfg), device, C.byref(h))
         if st != 0:
@@ -172,7 +173,7 @@ class Context:
         if not on_dev:
             n0 = _host(n0)
         rows = n0.shape[0] if n0.ndim == 2 else 1
-        stride = 0 if rows == 1 else self.cfg.n_bins
+        stride = 0 if rows == 1 else self.cfg.n_bins * max(self.cfg.n_bins2, 1)
         c0 = _host(np.atleast_1d(c0))
         ts = _host(t_samples) if t_samples is not None else np.zeros(1)
         tg = _host(target)
@@ -188,17 +189,18 @@ class Context:
         """Records of the last run.  `out` may supply preallocated destinations (e.g. pinned
         host tensors' numpy views) with keys moments/status/steps/loss."""
         S, M = self.n_sims, self.cfg.n_samples
+        RW = 8 if self.cfg.n_bins2 > 0 else 6
         if out is not None:
             pass
         elif on_device:
             import torch
             dev = torch.device("cuda", self.device)
-            out = dict(moments=torch.empty((S, M, 6), dtype=torch.float64, device=dev),
+            out = dict(moments=torch.empty((S, M, RW), dtype=torch.float64, device=dev),
                        status=torch.empty(S, dtype=torch.int32, device=dev),
                        steps=torch.empty(S, dtype=torch.int64, device=dev),
                        loss=torch.empty(S, dtype=torch.float64, device=dev))
         else:
-            out = dict(moments=np.empty((S, M, 6)), status=np.empty(S, np.int32), steps=np.empty(S, np.int64),
+            out = dict(moments=np.empty((S, M, RW)), status=np.empty(S, np.int32), steps=np.empty(S, np.int64),
                        loss=np.empty(S))
         self._check(self._lib.pbe_moments(self._h, _ptr(out.get("moments")), _ptr(out.get("status")),
                                           _ptr(out.get("steps")), _ptr(out.get("loss")), 1 if on_device else 0))
@@ -231,7 +233,8 @@ def context_for(w, kernel: int = KERNEL_AUTO, device: int = 0, max_sims: Optiona
     ctx = Context(w.N, w.dL, L_lo=w.L_lo, limiter=w.limiter, courant=w.courant, dt_fixed=w.dt_fixed,
                   dt_max=w.dt_max, max_steps=w.max_steps, n_steps=w.n_steps, rho_c=w.rho_c, k_v=w.k_v,
                   n_samples=w.M, n_tangents=w.n_tangents, max_sims=max_sims or w.n_sims, kernel=kernel,
-                  device=device)
+                  device=device, n_bins2=getattr(w, "N2", 0), L2_lo=getattr(w, "L2_lo", 0.0),
+                  dL2=getattr(w, "dL2", 0.0))
     ctx.set_kinetics(w.law, w.theta, w.sol_kind, w.sol, w.knot_t, w.knot_T, w.tangent_seed)
     return ctx
 
@@ -243,7 +246,8 @@ def run_workload(w, kernel: int = KERNEL_AUTO, device: int = 0, want_n: bool = T
     dev = torch.device("cuda", device)
     ctx = context_for(w, kernel=kernel, device=device)
     n0 = w.n0 if host_n0 else torch.from_numpy(np.ascontiguousarray(w.n0)).to(dev)
-    nf = torch.empty((w.n_sims, w.N), dtype=torch.float64, device=dev) if want_n else None
+    cells = w.N * max(getattr(w, "N2", 0), 1)
+    nf = torch.empty((w.n_sims, cells), dtype=torch.float64, device=dev) if want_n else None
     ndf = (torch.empty((w.n_sims, w.n_tangents, w.N), dtype=torch.float64, device=dev)
            if (want_n and w.n_tangents) else None)
     ctx.run_batch(n0, w.c0, w.t_samples if w.n_steps == 0 else None, w.target, nf, ndf)

@@ -18,6 +18,7 @@
 #include "pbe_device.cuh"
 #include "k_resident.cuh"
 #include "k_stream.cuh"
+#include "k_2d.cuh"
 
 using pbe::KParams;
 
@@ -264,6 +265,61 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
 }
 
 // ------------------------------------------------------------------------------------
+// k_2d launch (NEXT-1): padded ping-pong planes, load kernel (+ mu12 partials), one
+// cooperative launch for the whole 2D march, store kernel for n_final.
+// ------------------------------------------------------------------------------------
+static pbe_status launch_2d(pbe_ctx ctx, KParams kp, int S, const double* f0, long long f0_stride,
+                            double* f_final, cudaStream_t st) {
+    const pbe_config& cf = ctx->cfg;
+    const int N1 = cf.n_bins, N2 = cf.n_bins2;
+    const long long P1 = 4LL * ((N1 + 3) / 4) + 4, R2 = 4LL * ((N2 + 3) / 4) + 4;
+    int sms = 0, per_sm = 0;
+    CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbe::k_2d, pbe::K2D_NT, 0));
+    if (per_sm < 1) return fail(ctx, PBE_ERR_CUDA, "k_2d does not fit on an SM");
+    per_sm = per_sm > 4 ? 4 : per_sm;
+    const unsigned G = (unsigned)(per_sm * sms);
+    const size_t plane = (size_t)R2 * P1, buf = (size_t)S * plane;
+    CUDA_TRY(ctx, ctx->sbuf.ensure(2 * buf * sizeof(double)));
+    CUDA_TRY(ctx, ctx->spart.ensure((size_t)S * G * 7 * sizeof(double)));
+    CUDA_TRY(ctx, ctx->sbar.ensure(8 * sizeof(unsigned)));
+    CUDA_TRY(ctx, ctx->snscale.ensure((size_t)S * sizeof(unsigned long long)));
+    double* A = ctx->sbuf.as<double>();
+    double* B = A + buf;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbuf.p, 0, 2 * buf * sizeof(double), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbar.p, 0, 8 * sizeof(unsigned), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->snscale.p, 0, (size_t)S * sizeof(unsigned long long), st));
+    pbe::k_2d_load<<<dim3(G, S), pbe::K2D_NT, 0, st>>>(f0, f0_stride, S, N1, N2, A, P1, R2, ctx->spart.as<double>(), G,
+                                                       ctx->snscale.as<unsigned long long>(), cf.L_lo, cf.dL, cf.L2_lo,
+                                                       cf.dL2);
+    CUDA_TRY(ctx, cudaGetLastError());
+    pbe::Params2D p2{};
+    p2.kp = kp;
+    p2.N2 = N2; p2.L2_lo = cf.L2_lo; p2.dL2 = cf.dL2; p2.inv_dL2 = 1.0 / cf.dL2;
+    p2.A = A; p2.B = B; p2.P1 = P1; p2.R2 = R2;
+    p2.part = ctx->spart.as<double>();
+    p2.bar = ctx->sbar.as<unsigned>();
+    p2.nscale_bits = ctx->snscale.as<unsigned long long>();
+    void* args[] = {&p2};
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)pbe::k_2d, dim3(G), dim3(pbe::K2D_NT), args, 0, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+    int launches = 2;
+    if (f_final) {
+        pbe::k_2d_store<<<2 * sms, 256, 0, st>>>(A, S, N1, N2, P1, R2, f_final);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
+    ctx->info.kernel = PBE_KERNEL_2D;
+    ctx->info.launches = launches;
+    ctx->info.threads_per_cta = pbe::K2D_NT;
+    ctx->info.ctas = (int)G;
+    ctx->info.cluster = 1;
+    ctx->info.bins_per_thread = pbe::K2D_K;
+    return PBE_OK;
+}
+
+// ------------------------------------------------------------------------------------
 // C ABI
 // ------------------------------------------------------------------------------------
 extern "C" {
@@ -291,7 +347,15 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (c.n_steps > 0 && c.n_samples != 1) return fail(nullptr, PBE_ERR_ARG, "steps mode needs n_samples == 1");
     if (c.n_tangents < 0 || c.n_tangents > pbe::MAXP) return fail(nullptr, PBE_ERR_ARG, "n_tangents must be in [0, 10]");
     if (c.max_sims < 1) return fail(nullptr, PBE_ERR_ARG, "max_sims must be >= 1");
-    if (c.kernel < PBE_KERNEL_AUTO || c.kernel > PBE_KERNEL_STREAM) return fail(nullptr, PBE_ERR_ARG, "unknown kernel %d", c.kernel);
+    if (c.kernel < PBE_KERNEL_AUTO || c.kernel > PBE_KERNEL_2D) return fail(nullptr, PBE_ERR_ARG, "unknown kernel %d", c.kernel);
+    if (c.n_bins2 < 0) return fail(nullptr, PBE_ERR_ARG, "n_bins2 must be >= 0");
+    if (c.n_bins2 > 0) {
+        if (c.n_bins2 < 3) return fail(nullptr, PBE_ERR_ARG, "n_bins2 must be >= 3 in 2D mode");
+        if (!(c.dL2 > 0.0) || !std::isfinite(c.dL2) || !std::isfinite(c.L2_lo))
+            return fail(nullptr, PBE_ERR_ARG, "dL2 must be finite and > 0 in 2D mode");
+        if (c.n_tangents != 0) return fail(nullptr, PBE_ERR_ARG, "2D mode has no tangent lanes (n_tangents = 0)");
+        if (c.max_sims > pbe::K2D_MAXS) return fail(nullptr, PBE_ERR_ARG, "2D mode: max_sims <= %d", pbe::K2D_MAXS);
+    }
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -308,7 +372,8 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     ctx->device = device;
     const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
     cudaError_t ea = cudaSuccess;
-    if (ea == cudaSuccess) ea = ctx->rec.ensure(S * M * 6 * sizeof(double));
+    const size_t RW = c.n_bins2 > 0 ? 8 : 6;                      // record width
+    if (ea == cudaSuccess) ea = ctx->rec.ensure(S * M * RW * sizeof(double));
     if (ea == cudaSuccess) ea = ctx->trec.ensure(S * M * (P ? P : 1) * 5 * sizeof(double));
     if (ea == cudaSuccess) ea = ctx->status.ensure(S * sizeof(int));
     if (ea == cudaSuccess) ea = ctx->steps.ensure(S * sizeof(long long));
@@ -347,9 +412,12 @@ pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t 
     if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
     if (law < PBE_LAW_CONST || law > PBE_LAW_POLY) return fail(ctx, PBE_ERR_ARG, "unknown law %d", law);
     if (n_params < 1 || n_params > pbe::MAXTH) return fail(ctx, PBE_ERR_ARG, "n_params must be in [1, 10]");
-    if (law == PBE_LAW_CONST && n_params != 1) return fail(ctx, PBE_ERR_ARG, "PBE_LAW_CONST takes 1 parameter");
-    if (law == PBE_LAW_ARRHENIUS_GD && n_params != 3 && n_params != 6)
-        return fail(ctx, PBE_ERR_ARG, "PBE_LAW_ARRHENIUS_GD takes 3 or 6 parameters");
+    const bool two_d = ctx->cfg.n_bins2 > 0;
+    if (two_d && (n_params % 2) != 0) return fail(ctx, PBE_ERR_ARG, "2D mode: theta = [dim-1 law | dim-2 law] (even n_params)");
+    const int per_dim = two_d ? n_params / 2 : n_params;
+    if (law == PBE_LAW_CONST && per_dim != 1) return fail(ctx, PBE_ERR_ARG, "PBE_LAW_CONST takes 1 parameter per dimension");
+    if (law == PBE_LAW_ARRHENIUS_GD && per_dim != 3 && per_dim != 6)
+        return fail(ctx, PBE_ERR_ARG, "PBE_LAW_ARRHENIUS_GD takes 3 or 6 parameters per dimension");
     if (n_sims < 1 || n_sims > ctx->cfg.max_sims) return fail(ctx, PBE_ERR_ARG, "n_sims must be in [1, max_sims]");
     if (!theta || !sol_params || !knot_t || !knot_T) return fail(ctx, PBE_ERR_ARG, "NULL kinetics array");
     if (sol_kind == PBE_SOL_EXP ? n_sol != 2 : (sol_kind == PBE_SOL_POLY ? n_sol != 3 : true))
@@ -396,7 +464,9 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     if (n_sims < 1 || n_sims > cf.max_sims) return fail(ctx, PBE_ERR_ARG, "n_sims must be in [1, max_sims]");
     if (n_sims != ctx->kin_sims) return fail(ctx, PBE_ERR_ARG, "n_sims (%d) != kinetics n_sims (%d)", n_sims, ctx->kin_sims);
     if (!n0 || !c0) return fail(ctx, PBE_ERR_ARG, "NULL n0 or c0");
-    if (n0_stride != 0 && n0_stride != N) return fail(ctx, PBE_ERR_ARG, "n0_stride must be 0 or n_bins");
+    const bool two_d = cf.n_bins2 > 0;
+    const long long cells = (long long)N * (two_d ? cf.n_bins2 : 1);
+    if (n0_stride != 0 && n0_stride != cells) return fail(ctx, PBE_ERR_ARG, "n0_stride must be 0 or the cells per simulation");
     if (!steps_mode && !t_samples) return fail(ctx, PBE_ERR_ARG, "NULL t_samples");
     for (int s = 0; s < n_sims; ++s)
         if (!(c0[s] >= 0.0) || !std::isfinite(c0[s])) return fail(ctx, PBE_ERR_ARG, "c0[%d] must be finite and >= 0", s);
@@ -408,7 +478,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     }
     if (!n0_on_device) {
         const size_t rows = n0_stride ? (size_t)n_sims : 1;
-        for (size_t j = 0; j < rows * N; ++j)
+        for (size_t j = 0; j < rows * (size_t)cells; ++j)
             if (!(n0[j] >= 0.0) || !std::isfinite(n0[j])) return fail(ctx, PBE_ERR_ARG, "n0[%zu] must be finite and >= 0", j);
     }
     if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
@@ -432,6 +502,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     if (kind == PBE_KERNEL_AUTO) kind = rv ? PBE_KERNEL_RESIDENT : (cv ? PBE_KERNEL_CLUSTER : PBE_KERNEL_STREAM);
     if (kind == PBE_KERNEL_CLUSTER && !cv)
         return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit a 16-CTA cluster", N, P);
+    if (two_d) kind = PBE_KERNEL_2D;
     if (kind == PBE_KERNEL_RESIDENT && !rv)
         return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit the resident kernel", N, P);
     if (kind == PBE_KERNEL_STREAM && !sv)
@@ -449,13 +520,13 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     }
     const double* n0_dev = n0;
     if (!n0_on_device) {
-        const size_t bytes = (n0_stride ? (size_t)n_sims : 1) * N * sizeof(double);
+        const size_t bytes = (n0_stride ? (size_t)n_sims : 1) * (size_t)cells * sizeof(double);
         CUDA_TRY(ctx, ctx->n0_staged.ensure(bytes));
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->n0_staged.p, n0, bytes, cudaMemcpyHostToDevice, st));
         n0_dev = ctx->n0_staged.as<double>();
     }
     // unreached samples read as NaN (all-ones bytes)
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->rec.p, 0xff, (size_t)n_sims * M * 6 * sizeof(double), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->rec.p, 0xff, (size_t)n_sims * M * (two_d ? 8 : 6) * sizeof(double), st));
     if (P) CUDA_TRY(ctx, cudaMemsetAsync(ctx->trec.p, 0xff, (size_t)n_sims * M * P * 5 * sizeof(double), st));
 
     KParams kp{};
@@ -474,7 +545,10 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     kp.n_final = n_final; kp.ndot_final = ndot_final;
 
     ctx->info = pbe_run_info{};
-    if (kind == PBE_KERNEL_RESIDENT) {
+    if (two_d) {
+        pbe_status r = launch_2d(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st);
+        if (r != PBE_OK) return r;
+    } else if (kind == PBE_KERNEL_RESIDENT) {
         const int nt = ((N + rv->K - 1) / rv->K + 31) / 32 * 32;
         const size_t smem = resident_smem(*rv, nt);
         CUDA_TRY(ctx, cudaFuncSetAttribute(rv->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -550,7 +624,8 @@ pbe_status pbe_moments(pbe_ctx ctx, double* moments, int32_t* sim_status, int64_
     pbe_status r = finish_run(ctx);
     if (r != PBE_OK) return r;
     const size_t S = ctx->last_sims, M = ctx->cfg.n_samples;
-    if ((r = copy_out(ctx, moments, ctx->rec.p, S * M * 6 * sizeof(double), on_device)) != PBE_OK) return r;
+    const size_t RW = ctx->cfg.n_bins2 > 0 ? 8 : 6;
+    if ((r = copy_out(ctx, moments, ctx->rec.p, S * M * RW * sizeof(double), on_device)) != PBE_OK) return r;
     if ((r = copy_out(ctx, sim_status, ctx->status.p, S * sizeof(int), on_device)) != PBE_OK) return r;
     if ((r = copy_out(ctx, sim_steps, ctx->steps.p, S * sizeof(long long), on_device)) != PBE_OK) return r;
     if ((r = copy_out(ctx, loss, ctx->loss.p, S * sizeof(double), on_device)) != PBE_OK) return r;

@@ -1,0 +1,59 @@
+"""NEXT-1 GPU parity: the 2D Godunov-split kernel (k_2d) vs the 2D oracle on the same seeded
+inputs.  Tolerances as for 1D: records 1e-10 relative, f 1e-9 max-abs relative to max f."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(w):
+    import paper_2411_00742_b200 as pb
+    o = oracle.run2d(w, threads=8)
+    g = pb.run_workload(w)
+    assert g["info"]["kernel"] == 4
+    assert np.array_equal(g["status"], o["status"]) and np.array_equal(g["steps"], o["steps"])
+    a, b = g["samples"], o["samples"]
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    ok = ~np.isnan(b)
+    assert np.max(np.abs(a[ok] - b[ok]) / np.abs(b[ok])) <= 1e-10
+    for s in range(w.n_sims):
+        if o["status"][s] == 0:
+            f = o["f_final"][s].reshape(-1)
+            assert np.max(np.abs(g["n_final"][s] - f)) <= 1e-9 * np.max(np.abs(f))
+    return g, o
+
+
+@pytest.mark.parametrize("lim", [W.LIM_UPWIND, W.LIM_VANLEER])
+def test_2d_base_case_coarse(lim):
+    _check(W.c2d_base(120, 60, t_max=20.0, M=10, limiter=lim))
+
+
+@pytest.mark.parametrize("N1,N2", [(61, 33), (97, 50), (240, 121)])
+def test_2d_ragged_grids(N1, N2):
+    _check(W.c2d_base(N1, N2, t_max=6.0, M=3))
+
+
+def test_2d_batch_temperatures_and_cap():
+    w = W.c2d_base(100, 50, t_max=15.0, M=5, n_sims=5, dt_max=0.05)
+    w.knot_T = np.array([[10.0], [12.0], [15.0], [18.0], [20.0]])
+    w.c0 = np.array([8.0, 7.5, 8.0, 9.0, 10.0])
+    _check(w)
+
+
+def test_2d_steps_mode_and_statuses():
+    w = W.c2d_base(80, 40, n_sims=3)
+    w.n_steps = 25
+    w.t_samples = np.array([1.0])
+    _check(w)
+    w = W.c2d_base(80, 40, t_max=30.0, M=3, n_sims=2)
+    w.c0 = np.array([8.0, 0.001])          # second simulation runs out of solute
+    w.max_steps = 10_000
+    _check(w)
+
+
+def test_2d_full_base_grid_sampled():
+    """Table 1 grid (1200 x 600 at 1 um) for 2 minutes of the march."""
+    _check(W.c2d_base(1200, 600, t_max=2.0, M=2))

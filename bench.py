@@ -59,6 +59,16 @@ def make_workload(name: str, world: int, args):
         w = W.c4_sweep(N, batch=b * world, n_steps=args.march_steps or 1000)
         desc = dict(workload=f"C4 bin sweep N={N} batch {b}/GPU", sims_per_gpu=b, bins=N,
                     march_steps=w.n_steps, limiter="van Leer", cfl="uncapped (C = 0.9)")
+    elif name == "c2d":
+        N1 = args.bins or 6000
+        N2 = args.bins2 or N1 // 2
+        b = args.batch or 1
+        w = W.c2d_base(N1, N2, n_sims=b * world)
+        w.n_steps = args.march_steps or 200
+        w.t_samples = np.array([1.0])
+        desc = dict(workload=f"NEXT-1 2D base case {N1}x{N2} (Table 1 grid x {1200 // N1 if N1 <= 1200 else 'fine'}), "
+                    f"Godunov splitting, {w.n_steps} uncapped CFL steps, {b} sim(s)/GPU", bins=N1 * N2,
+                    sims_per_gpu=b, march_steps=w.n_steps, limiter="van Leer")
     elif name == "c3":
         w = W.c3_cycling()
         desc = dict(workload="C3 temperature cycling (single sim; replicas only)", bins=1000, march_steps=100000)
@@ -194,7 +204,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c2d"])
+    ap.add_argument("--bins2", type=int, default=0, help="2D: bins along L2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--bins", type=int, default=0, help="C4: bins per simulation")
     ap.add_argument("--batch", type=int, default=0, help="C4: simulations per GPU")
@@ -265,7 +276,7 @@ def main():
         torch.cuda.synchronize(dev)
         res = ctx.moments()
         assert np.all(res["status"] == 0), f"simulation failures: {np.unique(res['status'])}"
-        bu = float(w.N) * float(np.sum(res["steps"]))
+        bu = float(w.N) * max(getattr(w, "N2", 0), 1) * float(np.sum(res["steps"]))
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         barrier()
         torch.cuda.synchronize(dev)
@@ -295,12 +306,12 @@ def main():
 
     def roofline(w, info, bu_local, kms, workload):
         P = w.n_tangents
-        if info["kernel"] == pb.KERNEL_STREAM:
-            bytes_per = 16.0 * (1 + P)
+        if info["kernel"] in (pb.KERNEL_STREAM, pb.KERNEL_2D):
+            bytes_per = 16.0 * (1 + P) * (2.0 if info["kernel"] == pb.KERNEL_2D else 1.0)   # 2D: two sweeps
             achieved = bytes_per * bu_local / (kms * 1e-3) / 1e9
             hbm = float(peaks.get("hbm_gbs", 6650.0))
             r = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm, traffic=None,
-                     kernel="k_stream", bytes_per_bin_update=bytes_per,
+                     kernel="k_2d" if info["kernel"] == pb.KERNEL_2D else "k_stream", bytes_per_bin_update=bytes_per,
                      peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s", kernel_ms=kms)
         else:
             f = flops_per_bin_update(w.limiter, P)
@@ -410,7 +421,7 @@ def main():
         cfg = dict(desc)
         cfg.update(parallelism=(f"sims sharded round-robin over {world} GPUs; NCCL allgather of per-sim records"
                                 if world > 1 else "1 GPU"), l2="flushed between timed iterations (512 MiB write)",
-                   steps_per_sim_mean=bu_local / w.N / max(w.n_sims, 1), kernel=info)
+                   steps_per_sim_mean=bu_local / (w.N * max(w.N2, 1)) / max(w.n_sims, 1), kernel=info)
         line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
                     ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
                     data="synthetic (seeded; DESIGN.md input recipe)", config=cfg, roofline=roof,

@@ -57,3 +57,16 @@ def test_2d_steps_mode_and_statuses():
 def test_2d_full_base_grid_sampled():
     """Table 1 grid (1200 x 600 at 1 um) for 2 minutes of the march."""
     _check(W.c2d_base(1200, 600, t_max=2.0, M=2))
+
+
+def test_2d_paper_step_count_6000x3000():
+    """PIN-16 (weak, paper-printed): the Table 1 base case on the 6000 x 3000 grid "required
+    1339 time steps" with uncapped CFL steps (nu = 0.9).  The number of steps
+    is the L1 growth distance / (nu dL1); the 2D method of moments gives 241-255 um, i.e.
+    1339-1417 steps.  Run to 1000 min (S -> 1) and compare within 6%."""
+    import paper_2411_00742_b200 as pb
+    w = W.c2d_base(6000, 3000, t_max=1000.0, M=1)
+    g = pb.run_workload(w, want_n=False)
+    assert g["status"][0] == 0
+    steps = int(g["steps"][0])
+    assert 1339 * 0.94 <= steps <= 1417 * 1.06, steps

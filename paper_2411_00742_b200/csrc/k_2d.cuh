@@ -62,7 +62,7 @@ __device__ __forceinline__ void line_update(const double (&w)[K2D_K + 4], double
     for (int k = 0; k < K2D_K; ++k) y[k] = w[k + 2] - (F[k + 1] - F[k]);
 }
 
-__global__ void __launch_bounds__(K2D_NT, 1) k_2d(const Params2D p2) {
+__global__ void __launch_bounds__(K2D_NT, 3) k_2d(const Params2D p2) {
     const KParams& kp = p2.kp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = K2D_NT / 32;

@@ -171,6 +171,8 @@ typedef struct {
     int32_t bins_per_thread; /* register-resident bins per thread (0 if streaming) */
     double  main_ms;         /* CUDA-event duration of the main kernel of the last run
                                 (measured on the launch stream; valid after pbe_moments) */
+    int32_t steps_per_pass;  /* time steps fused per HBM pass (k_stream temporal blocking, NEXT-4;
+                                1 otherwise) */
 } pbe_run_info;
 pbe_status pbe_last_run_info(pbe_ctx ctx, pbe_run_info* info);
 

@@ -1,0 +1,328 @@
+// =====================================================================================
+//  k_stream_tb — NEXT-4: temporal blocking of uncapped CFL steps in the HBM-streaming march
+//  (steps mode, dt_max = inf, no fixed dt, primal only; BASELINE config C4).
+//
+//  In an uncapped CFL step the Courant number is C = nu sgn(G) EXACTLY (R-9), so the sweep
+//  depends on the kinetics only through the sign of G.  While that sign is unchanged, KB
+//  consecutive steps are the same geometric update and can be fused per HBM pass:
+//
+//    per tile: one TMA bulk load of tile + GH = 2 KB ghost-width halo cells per side, d <= KB
+//      sub-steps in shared memory (the halo's garbage front moves 2 cells per sub-step and
+//      never reaches the owned cells), per-sub-step mu3 partials of the owned cells, one
+//      16-byte store of the owned cells after the last sub-step
+//    grid barrier
+//    scalar phase (one warp per simulation, fixed order): replay the d sub-steps: mass
+//      balance c^{n+1} = c^n - rho_c k_v (mu3^{n+1} - mu3^n) (L304-312), S, G, the clock
+//      t += nu dL/|G| (SI L859); if sgn G changes inside the block the block is valid only up
+//      to that sub-step: the simulation keeps its buffer and redoes that prefix (bitwise the
+//      same sub-steps), then continues with the new sign.  Each simulation owns its buffer
+//      parity and block depth, so no global consensus is needed.
+//
+//  Algorithmic traffic per bin-update: 16 B / d (one read + one write per d steps).
+// =====================================================================================
+#pragma once
+#include "k_2d.cuh"      // line_update<NEG> (K = 4 cells from an 8-cell window)
+#include "k_stream.cuh"
+
+namespace pbe {
+
+constexpr int TB_KB = 8;                 // max fused steps per block
+constexpr int TB_GH = 2 * TB_KB;         // ghost / halo width (cells)
+constexpr int TB_STAGES = 2;
+constexpr int TB_NWC = 8;
+constexpr int TB_NT = 32 * (TB_NWC + 1);
+
+struct StreamTBParams {
+    KParams kp;
+    double* buf0;            // [S][pitch], bin i at index i + TB_GH
+    double* buf1;
+    long long pitch;
+    int TB, T_sim;
+    long long n_tiles;
+    double* part;            // [S][T_sim][NWC][KB][5]  (mu0..mu3, negative flag) per sub-step
+    unsigned* bar;
+    int* active;
+    int* final_buf;          // [S]
+    const unsigned long long* nscale_bits;
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(TB_NT, 1) k_stream_tb(const StreamTBParams sp) {
+    constexpr int KB = TB_KB, GH = TB_GH, NWC = TB_NWC, K = 4;
+    const KParams& kp = sp.kp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = (warp == NWC);
+    const int N = kp.N, TB = sp.TB;
+    const int WL = TB + 2 * GH;                       // window length (cells)
+    const unsigned G = gridDim.x;
+    const bool vl = kp.limiter == LIM_VANLEER;
+    const double L_half = kp.L_lo + 0.5 * kp.dL;
+
+    const long long t_lo = (sp.n_tiles * blockIdx.x) / G;
+    const long long t_hi = (sp.n_tiles * (blockIdx.x + 1)) / G;
+    const int s_lo = (int)(t_lo / sp.T_sim);
+    const int ns = (t_hi > t_lo) ? (int)((t_hi - 1) / sp.T_sim) - s_lo + 1 : 0;
+
+    extern __shared__ __align__(128) double smem[];   // [STAGES][WL] stage, [2][WL] work
+    double* work0 = smem + (size_t)TB_STAGES * WL;
+    double* work1 = work0 + WL;
+    __shared__ __align__(8) unsigned long long s_full[TB_STAGES], s_empty[TB_STAGES];
+
+    struct SimS {
+        double c, t, mu3p, clip, G;     // G: growth rate at the start of the next block
+        long long nstep;
+        int status, cur, depth, sign, active, sample;
+    };
+    __shared__ SimS s_sim[STREAM_MAXS];
+
+    if (tid == 0)
+        for (int i = 0; i < TB_STAGES; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], NWC); }
+    for (int x = tid; x < 2 * WL; x += TB_NT) work0[x] = 0.0;      // edge cells are read, never used
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    // growth rate at concentration c (primal; T constant or profile at time t)
+    auto growth = [&](int s, double c, double t) -> double {
+        const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, -1, kp.n_params, kp.n_params + kp.n_sol};
+        const double* kT = kp.knot_T + (size_t)s * kp.knotT_stride;
+        const KinCache KC = kin_cache(kp, KL, kT);
+        D1 T;
+        const D1 S = supersaturation(kp, KL, kT, KC, mk(t), mk(c), T);
+        const double g = growth_rate(kp, KL, S, T).v;
+        return fabs(g) > 1e-300 ? g : 0.0;
+    };
+    auto sgn = [](double g) { return g > 0.0 ? 1 : (g < 0.0 ? -1 : 0); };
+
+    // ---- init: mu3(n0) from the load kernel's per-tile partials (sub-step 0 slot) --------------
+    auto sum_sub = [&](int s, int q, int km) -> double {    // fixed order: lanes, then xor tree
+        const double* pt = sp.part + (size_t)s * sp.T_sim * NWC * KB * 5;
+        const int ne = sp.T_sim * NWC;
+        double a = 0.0;
+        for (int e = lane; e < ne; e += 32) a += pt[((size_t)e * KB + q) * 5 + km];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        return a;
+    };
+    if (warp < ns) {
+        const int s = s_lo + warp;
+        SimS W{};
+        W.c = kp.c0[s]; W.t = 0.0; W.mu3p = sum_sub(s, 0, 3); W.nstep = 0; W.status = ST_OK; W.cur = 0;
+        W.clip = 1e-12 * __longlong_as_double((long long)sp.nscale_bits[s]);
+        W.G = growth(s, W.c, W.t);
+        W.sign = sgn(W.G);
+        W.active = kp.n_steps > 0 && kp.max_steps > 0;
+        if (kp.max_steps <= 0) W.status = ST_MAXSTEPS;
+        W.depth = (int)min((long long)KB, kp.n_steps);
+        W.sample = W.depth == kp.n_steps;
+        if (lane == 0) s_sim[warp] = W;
+    }
+    __syncthreads();
+
+    unsigned gen = 0;
+    long long n = 0;
+    unsigned long long qq = 0;
+    auto tile_active = [&](long long t) { return s_sim[(int)(t / sp.T_sim) - s_lo].active != 0; };
+    auto next_active = [&](long long t) { while (t < t_hi && !tile_active(t)) ++t; return t; };
+    while (true) {
+        if (producer) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                unsigned long long q = qq;
+                for (long long t = next_active(t_lo); t < t_hi; t = next_active(t + 1), ++q) {
+                    const int st = (int)(q % TB_STAGES);
+                    if (q >= TB_STAGES) mbar_wait(&s_empty[st], (unsigned)(((q / TB_STAGES) - 1) & 1));
+                    const int s = (int)(t / sp.T_sim), j = (int)(t - (long long)s * sp.T_sim);
+                    const int b0 = j * TB;
+                    const double* src = s_sim[s - s_lo].cur ? sp.buf1 : sp.buf0;
+                    const unsigned bytes = (unsigned)WL * 8u;               // [b0 - GH, b0 + TB + GH)
+                    mbar_expect_tx(&s_full[st], bytes);
+                    bulk_g2s(smem + (size_t)st * WL, src + (size_t)s * sp.pitch + b0, bytes, &s_full[st]);
+                }
+            }
+            for (long long t = next_active(t_lo); t < t_hi; t = next_active(t + 1)) ++qq;
+        } else {
+            for (long long t = next_active(t_lo); t < t_hi; t = next_active(t + 1), ++qq) {
+                const int st = (int)(qq % TB_STAGES);
+                mbar_wait(&s_full[st], (unsigned)((qq / TB_STAGES) & 1));
+                const int s = (int)(t / sp.T_sim), j = (int)(t - (long long)s * sp.T_sim);
+                const int b0 = j * TB, nb = min(TB, N - b0);
+                const SimS& W = s_sim[s - s_lo];
+                const int d = W.depth, sgn_b = W.sign;
+                const bool sample_last = W.sample != 0;
+                const double C = sgn_b * kp.courant, aC = fabs(C), kap2 = aC * (1.0 - aC);
+                const double thr = W.clip;
+                const double* in = smem + (size_t)st * WL;
+                double* outb = work0;
+                double* dst = (W.cur ? sp.buf0 : sp.buf1) + (size_t)s * sp.pitch + b0 + GH;
+                for (int q = 0; q < d; ++q) {
+                    const bool last = (q == d - 1);
+                    const bool all_mom = last && sample_last;
+                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                    bool bad = false;
+                    // cells x = 2 .. WL-3 of the window (global bin b0 - GH + x)
+                    for (int x0 = 2 + (warp * 32 + lane) * K; x0 < WL - 2; x0 += NWC * 32 * K) {
+                        double w[K + 4];
+#pragma unroll
+                        for (int r = 0; r < K + 4; ++r) w[r] = (x0 - 2 + r < WL) ? in[x0 - 2 + r] : 0.0;
+                        double y[K];
+                        if (C >= 0.0) line_update<false>(w, C, kap2, vl, y);
+                        else          line_update<true>(w, C, kap2, vl, y);
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const int x = x0 + k;
+                            const int i = b0 - GH + x;                       // global bin
+                            double v = y[k];
+                            if (i < 0 || i >= N || x >= WL - 2) v = 0.0;     // ghosts stay zero
+                            else if (v < 0.0) { if (v >= -thr) v = 0.0; else if (x >= GH && x < GH + nb) bad = true; }
+                            y[k] = v;
+                            if (x >= GH && x < GH + nb) {                    // owned cell: partials
+                                const double Lc = fma((double)i, kp.dL, L_half);
+                                const double w1 = kp.dL * Lc, w2 = w1 * Lc;
+                                acc[3] = fma(w2 * Lc, v, acc[3]);
+                                if (all_mom) { acc[0] = fma(kp.dL, v, acc[0]); acc[1] = fma(w1, v, acc[1]); acc[2] = fma(w2, v, acc[2]); }
+                                if (last) dst[x - GH] = v;                   // owned cells after d sub-steps
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+                            if (x0 + k < WL) outb[x0 + k] = y[k];
+                    }
+                    if (q == 0) { __syncwarp(); if (lane == 0) mbar_arrive(&s_empty[st]); }   // stage consumed
+                    // per-warp partials of sub-step q
+                    double* pt = sp.part + ((((size_t)s * sp.T_sim + j) * NWC + warp) * KB + q) * 5;
+#pragma unroll
+                    for (int km = 0; km < 4; ++km) {
+                        if (km == 3 || all_mom) {
+                            double r = acc[km];
+#pragma unroll
+                            for (int off = 16; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+                            if (lane == 0) pt[km] = r;
+                        }
+                    }
+                    const bool bany = __any_sync(0xffffffffu, bad);
+                    if (lane == 0) pt[4] = bany ? 1.0 : 0.0;
+                    named_bar(1, NWC * 32);                 // sub-step q complete in smem
+                    in = outb;
+                    outb = (outb == work0) ? work1 : work0;
+                }
+            }
+        }
+
+        // ---- grid barrier + active count ------------------------------------------------------
+        if (tid == 0) {
+            int mine = 0;
+            for (int slot = 0; slot < ns; ++slot)
+                if ((long long)(s_lo + slot) * sp.T_sim >= t_lo && s_sim[slot].active) ++mine;
+            if (mine) atomicAdd(&sp.active[n % 3], mine);
+        }
+        grid_sync(sp.bar, G, gen);
+        const int still = *((volatile int*)&sp.active[n % 3]);
+        if (blockIdx.x == 0 && tid == 0) sp.active[(n + 2) % 3] = 0;
+        if (still == 0) break;
+
+        // ---- scalar phase: replay the block's sub-steps (one warp per simulation) --------------
+        if (warp < ns && s_sim[warp].active) {
+            const int slot = warp, s = s_lo + slot;
+            const bool owner = (long long)s * sp.T_sim >= t_lo;
+            const SimS W0 = s_sim[slot];
+            SimS W = W0;
+            const int d = W.depth;
+            int valid = d;
+            double mu[4] = {0.0, 0.0, 0.0, 0.0};
+            bool fail = false;
+            for (int q = 0; q < d; ++q) {
+                const double mu3n = sum_sub(s, q, 3);
+                const double badf = sum_sub(s, q, 4);
+                const double cn = W.c - kp.rho_kv * (mu3n - W.mu3p);
+                // clock of this sub-step: uncapped CFL dt = nu dL / |G| (0 when G = 0, steps mode)
+                const double dt = W.G != 0.0 ? (kp.courant * kp.dL) * rcp_nr(fabs(W.G)) : 0.0;
+                if (badf > 0.0) { W.status = ST_NEG; fail = true; valid = q + 1; break; }
+                if (cn < 0.0) { W.status = ST_INFEAS; fail = true; valid = q + 1; break; }
+                W.c = cn; W.mu3p = mu3n; W.t += dt; ++W.nstep;
+                W.G = growth(s, W.c, W.t);
+                if (q + 1 < d && sgn(W.G) != W.sign) { valid = q + 1; break; }   // sign change inside
+            }
+            if (!fail && valid < d) {
+                // redo the valid prefix from the unchanged buffer (bitwise the same sub-steps)
+                W = W0;
+                W.depth = valid;
+                W.sample = W0.sample && false;
+            } else {
+                if (W.sample && owner && !fail) {
+                    for (int km = 0; km < 4; ++km) mu[km] = sum_sub(s, d - 1, km);
+                    if (lane == 0) {
+                        double* r = kp.rec + (size_t)s * kp.M * 6;
+                        r[0] = W.t; r[1] = W.c; r[2] = mu[0]; r[3] = mu[1]; r[4] = mu[2]; r[5] = mu[3];
+                    }
+                }
+                W.cur ^= 1;                                  // the block's result is the current state
+                if (fail || W.nstep >= kp.n_steps) W.active = 0;
+                else if (W.nstep >= kp.max_steps) { W.status = ST_MAXSTEPS; W.active = 0; }
+                else {
+                    W.sign = sgn(W.G);
+                    W.depth = (int)min((long long)KB, kp.n_steps - W.nstep);
+                    W.sample = (W.nstep + W.depth == kp.n_steps);
+                }
+                if (!W.active && owner && lane == 0) sp.final_buf[s] = W.cur;
+            }
+            __syncwarp();
+            if (lane == 0) s_sim[slot] = W;
+        }
+        __syncthreads();
+        ++n;
+    }
+    if (warp < ns) {
+        const int s = s_lo + warp;
+        if ((long long)s * sp.T_sim >= t_lo && lane == 0) {
+            const SimS W = s_sim[warp];
+            kp.status[s] = W.status;
+            kp.steps[s] = W.nstep;
+            if (kp.loss) kp.loss[s] = __longlong_as_double(0x7ff8000000000000ll);
+            if (W.nstep == 0) sp.final_buf[s] = 0;
+        }
+    }
+}
+
+// n0 -> buffer 0 (index i + GH), mu3(n0) partials per tile in sub-step slot 0, max(n0) bits
+__global__ void __launch_bounds__(256) k_stream_tb_load(const double* __restrict__ n0, long long n0_stride, int N,
+                                                        double* __restrict__ buf, long long pitch, unsigned long long* nscale_bits,
+                                                        int TB, int T_sim, double* __restrict__ part, double L_lo, double dL) {
+    const int s = blockIdx.y, j = blockIdx.x;
+    const int b0 = j * TB, nb = min(TB, N - b0);
+    double m = 0.0, a3 = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        const int i = b0 + k;
+        const double v = n0[(size_t)s * n0_stride + i];
+        buf[(size_t)s * pitch + TB_GH + i] = v;
+        m = fmax(m, v);
+        const double Lc = fma((double)i, dL, L_lo + 0.5 * dL);
+        a3 = fma(dL * Lc * Lc * Lc, v, a3);
+    }
+    __shared__ double s_a[8], s_m[8];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+    }
+    if ((threadIdx.x & 31) == 0) { s_a[threadIdx.x >> 5] = a3; s_m[threadIdx.x >> 5] = m; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, mm = 0.0;
+        for (int w = 0; w < 8; ++w) { t += s_a[w]; mm = fmax(mm, s_m[w]); }
+        double* pt = part + ((size_t)s * T_sim + j) * TB_NWC * TB_KB * 5;
+        for (int e = 0; e < TB_NWC * TB_KB * 5; ++e) pt[e] = 0.0;
+        pt[3] = t;                                   // warp 0, sub-step 0, mu3
+        atomicMax(nscale_bits + s, (unsigned long long)__double_as_longlong(mm));
+    }
+}
+
+__global__ void k_stream_tb_store(const double* __restrict__ buf0, const double* __restrict__ buf1,
+                                  const int* __restrict__ final_buf, int N, long long pitch, double* __restrict__ n_final) {
+    const int s = blockIdx.y;
+    const double* b = final_buf[s] ? buf1 : buf0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+        n_final[(size_t)s * N + i] = b[(size_t)s * pitch + TB_GH + i];
+}
+
+}  // namespace pbe

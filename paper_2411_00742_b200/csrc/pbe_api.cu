@@ -19,6 +19,7 @@
 #include "k_resident.cuh"
 #include "k_stream.cuh"
 #include "k_2d.cuh"
+#include "k_stream_tb.cuh"
 
 using pbe::KParams;
 
@@ -68,6 +69,7 @@ struct pbe_ctx_s {
     int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
     bool cluster2 = false;   // env PBE_CLUSTER2: 2-CTA clusters at 2 CTAs/SM for small N
     int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
+    bool temporal_block = true;  // env PBE_TEMPORAL_BLOCK=0 disables NEXT-4 in k_stream
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {
@@ -265,6 +267,71 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
 }
 
 // ------------------------------------------------------------------------------------
+// k_stream_tb launch (NEXT-4): temporal blocking of uncapped CFL steps (steps mode, primal)
+// ------------------------------------------------------------------------------------
+static pbe_status launch_stream_tb(pbe_ctx ctx, KParams kp, int S, const double* n0, long long n0_stride,
+                                   double* n_final, cudaStream_t st) {
+    const int N = kp.N;
+    const int TB = pbe::stream_tile(N, 1);
+    const int T_sim = (N + TB - 1) / TB;
+    const long long pitch = ((long long)T_sim * TB + 2 * pbe::TB_GH + 3) / 4 * 4;
+    int sms = 0, per_sm = 0;
+    CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int WL = TB + 2 * pbe::TB_GH;
+    const size_t smem = (size_t)(pbe::TB_STAGES + 2) * WL * sizeof(double);
+    CUDA_TRY(ctx, cudaFuncSetAttribute((const void*)pbe::k_stream_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbe::k_stream_tb, pbe::TB_NT, smem));
+    if (per_sm < 1) return fail(ctx, PBE_ERR_CUDA, "k_stream_tb does not fit on an SM (smem %zu)", smem);
+    per_sm = per_sm > 2 ? 2 : per_sm;
+    const int G = per_sm * sms;
+    const long long n_tiles = (long long)S * T_sim;
+    const long long chunk = (n_tiles + G - 1) / G;
+    if ((chunk + T_sim - 1) / T_sim + 1 > pbe::STREAM_MAXS)
+        return fail(ctx, PBE_ERR_ARG, "too many simulations per CTA for the streaming kernel (S = %d, N = %d)", S, N);
+    const size_t buf_el = (size_t)S * pitch;
+    CUDA_TRY(ctx, ctx->sbuf.ensure(2 * buf_el * sizeof(double)));
+    CUDA_TRY(ctx, ctx->spart.ensure((size_t)S * T_sim * pbe::TB_NWC * pbe::TB_KB * 5 * sizeof(double)));
+    CUDA_TRY(ctx, ctx->sbar.ensure(8 * sizeof(unsigned)));
+    CUDA_TRY(ctx, ctx->sfinal.ensure((size_t)S * sizeof(int)));
+    CUDA_TRY(ctx, ctx->snscale.ensure((size_t)S * sizeof(unsigned long long)));
+    double* b0 = ctx->sbuf.as<double>();
+    double* b1 = b0 + buf_el;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbuf.p, 0, 2 * buf_el * sizeof(double), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbar.p, 0, 8 * sizeof(unsigned), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->snscale.p, 0, (size_t)S * sizeof(unsigned long long), st));
+    pbe::k_stream_tb_load<<<dim3(T_sim, S), 256, 0, st>>>(n0, n0_stride, N, b0, pitch, ctx->snscale.as<unsigned long long>(),
+                                                          TB, T_sim, ctx->spart.as<double>(), kp.L_lo, kp.dL);
+    CUDA_TRY(ctx, cudaGetLastError());
+    pbe::StreamTBParams sp{};
+    sp.kp = kp;
+    sp.buf0 = b0; sp.buf1 = b1; sp.pitch = pitch; sp.TB = TB; sp.T_sim = T_sim; sp.n_tiles = n_tiles;
+    sp.part = ctx->spart.as<double>();
+    sp.bar = ctx->sbar.as<unsigned>();
+    sp.active = reinterpret_cast<int*>(ctx->sbar.as<unsigned>() + 4);
+    sp.final_buf = ctx->sfinal.as<int>();
+    sp.nscale_bits = ctx->snscale.as<unsigned long long>();
+    void* args[] = {&sp};
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)pbe::k_stream_tb, dim3(G), dim3(pbe::TB_NT), args, smem, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+    int launches = 2;
+    if (n_final) {
+        const dim3 lg((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, S);
+        pbe::k_stream_tb_store<<<lg, 256, 0, st>>>(b0, b1, sp.final_buf, N, pitch, n_final);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
+    ctx->info.kernel = PBE_KERNEL_STREAM;
+    ctx->info.launches = launches;
+    ctx->info.threads_per_cta = pbe::TB_NT;
+    ctx->info.ctas = G;
+    ctx->info.cluster = 1;
+    ctx->info.bins_per_thread = 0;
+    ctx->info.steps_per_pass = pbe::TB_KB;
+    return PBE_OK;
+}
+
+// ------------------------------------------------------------------------------------
 // k_2d launch (NEXT-1): padded ping-pong planes, load kernel (+ mu12 partials), one
 // cooperative launch for the whole 2D march, store kernel for n_final.
 // ------------------------------------------------------------------------------------
@@ -369,6 +436,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (const char* e = getenv("PBE_LANES_PER_CTA")) ctx->group_max = atoi(e);
     if (const char* e = getenv("PBE_CLUSTER2")) ctx->cluster2 = atoi(e) != 0;
     if (const char* e = getenv("PBE_RESIDENT_K")) ctx->resident_k = atoi(e);
+    if (const char* e = getenv("PBE_TEMPORAL_BLOCK")) ctx->temporal_block = atoi(e) != 0;
     ctx->device = device;
     const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
     cudaError_t ea = cudaSuccess;
@@ -545,6 +613,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     kp.n_final = n_final; kp.ndot_final = ndot_final;
 
     ctx->info = pbe_run_info{};
+    ctx->info.steps_per_pass = 1;
     if (two_d) {
         pbe_status r = launch_2d(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st);
         if (r != PBE_OK) return r;
@@ -589,6 +658,9 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
         ctx->info.ctas = n_sims * cs;
         ctx->info.cluster = cs;
         ctx->info.bins_per_thread = cv->K;
+    } else if (ctx->temporal_block && steps_mode && cf.dt_fixed == 0.0 && std::isinf(cf.dt_max) && P == 0) {
+        pbe_status r = launch_stream_tb(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st);
+        if (r != PBE_OK) return r;
     } else {
         pbe_status r = launch_stream(ctx, *sv, kp, n_sims, n0_dev, n0_stride, st);
         if (r != PBE_OK) return r;

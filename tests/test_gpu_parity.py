@@ -280,3 +280,23 @@ def test_cluster_statuses():
     w.c0 = w.c0.copy(); w.c0[2] = 0.001
     w.max_steps = 30
     _cluster(w)
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-4: temporal blocking of uncapped CFL steps in k_stream (steps mode, primal)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("N,batch,steps", [(4000, 3, 7), (4000, 3, 8), (9001, 2, 61), (30000, 5, 100)])
+def test_temporal_blocking_matches_oracle(N, batch, steps):
+    import paper_2411_00742_b200 as pb
+    g, o = _check(W.c4_sweep(N, batch=batch, n_steps=steps), kernel=pb.KERNEL_STREAM)
+    assert g["info"]["steps_per_pass"] == 8
+
+
+def test_temporal_blocking_sign_flips_redo():
+    """Supersaturation barely above 1: G changes sign every one or two steps, so most 8-step
+    blocks are invalidated and their valid prefix is redone (bitwise the same sub-steps)."""
+    import paper_2411_00742_b200 as pb
+    w = W.c4_sweep(4000, batch=3, n_steps=40)
+    w.c0 = np.array([5.782943125562973 * 1.0003, 5.782943125562973 * 1.001, 8.0])
+    g, o = _check(w, kernel=pb.KERNEL_STREAM)
+    assert g["info"]["steps_per_pass"] == 8

@@ -31,6 +31,8 @@ constexpr int TB_GH = 2 * TB_KB;         // ghost / halo width (cells)
 constexpr int TB_STAGES = 2;
 constexpr int TB_NWC = 8;
 constexpr int TB_NT = 32 * (TB_NWC + 1);
+// tile size of the temporal-blocking kernel (a function of N only: batch-independent sums)
+__host__ __device__ inline int stream_tb_tile(int N) { return N >= 2048 * 64 ? 2048 : (N >= 1024 * 64 ? 1024 : 512); }
 
 struct StreamTBParams {
     KParams kp;
@@ -48,7 +50,7 @@ struct StreamTBParams {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__global__ void __launch_bounds__(TB_NT, 1) k_stream_tb(const StreamTBParams sp) {
+__global__ void __launch_bounds__(TB_NT, 2) k_stream_tb(const StreamTBParams sp) {
     constexpr int KB = TB_KB, GH = TB_GH, NWC = TB_NWC, K = 4;
     const KParams& kp = sp.kp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -163,8 +165,12 @@ __global__ void __launch_bounds__(TB_NT, 1) k_stream_tb(const StreamTBParams sp)
                     // cells x = 2 .. WL-3 of the window (global bin b0 - GH + x)
                     for (int x0 = 2 + (warp * 32 + lane) * K; x0 < WL - 2; x0 += NWC * 32 * K) {
                         double w[K + 4];
+                        const double2* w2 = reinterpret_cast<const double2*>(in + x0 - 2);   // 16-byte aligned
 #pragma unroll
-                        for (int r = 0; r < K + 4; ++r) w[r] = (x0 - 2 + r < WL) ? in[x0 - 2 + r] : 0.0;
+                        for (int r = 0; r < (K + 4) / 2; ++r) {
+                            const double2 v2 = (x0 - 2 + 2 * r < WL) ? w2[r] : make_double2(0.0, 0.0);
+                            w[2 * r] = v2.x; w[2 * r + 1] = v2.y;
+                        }
                         double y[K];
                         if (C >= 0.0) line_update<false>(w, C, kap2, vl, y);
                         else          line_update<true>(w, C, kap2, vl, y);

@@ -272,7 +272,7 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
 static pbe_status launch_stream_tb(pbe_ctx ctx, KParams kp, int S, const double* n0, long long n0_stride,
                                    double* n_final, cudaStream_t st) {
     const int N = kp.N;
-    const int TB = pbe::stream_tile(N, 1);
+    const int TB = pbe::stream_tb_tile(N);
     const int T_sim = (N + TB - 1) / TB;
     const long long pitch = ((long long)T_sim * TB + 2 * pbe::TB_GH + 3) / 4 * 4;
     int sms = 0, per_sm = 0;

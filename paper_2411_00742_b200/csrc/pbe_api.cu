@@ -69,7 +69,8 @@ struct pbe_ctx_s {
     int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
     bool cluster2 = false;   // env PBE_CLUSTER2: 2-CTA clusters at 2 CTAs/SM for small N
     int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
-    bool temporal_block = true;  // env PBE_TEMPORAL_BLOCK=0 disables NEXT-4 in k_stream
+    bool temporal_block = false; // env PBE_TEMPORAL_BLOCK=1 enables NEXT-4 in k_stream (opt-in:
+                                 // correct, but slower than plain streaming for batches so far)
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {

@@ -285,14 +285,19 @@ def test_cluster_statuses():
 # ---------------------------------------------------------------------------------------
 # NEXT-4: temporal blocking of uncapped CFL steps in k_stream (steps mode, primal)
 # ---------------------------------------------------------------------------------------
+@pytest.fixture
+def temporal_blocking(monkeypatch):
+    monkeypatch.setenv("PBE_TEMPORAL_BLOCK", "1")     # read by pbe_create
+
+
 @pytest.mark.parametrize("N,batch,steps", [(4000, 3, 7), (4000, 3, 8), (9001, 2, 61), (30000, 5, 100)])
-def test_temporal_blocking_matches_oracle(N, batch, steps):
+def test_temporal_blocking_matches_oracle(N, batch, steps, temporal_blocking):
     import paper_2411_00742_b200 as pb
     g, o = _check(W.c4_sweep(N, batch=batch, n_steps=steps), kernel=pb.KERNEL_STREAM)
     assert g["info"]["steps_per_pass"] == 8
 
 
-def test_temporal_blocking_sign_flips_redo():
+def test_temporal_blocking_sign_flips_redo(temporal_blocking):
     """Supersaturation barely above 1: G changes sign every one or two steps, so most 8-step
     blocks are invalidated and their valid prefix is redone (bitwise the same sub-steps)."""
     import paper_2411_00742_b200 as pb

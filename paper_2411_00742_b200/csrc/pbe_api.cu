@@ -19,6 +19,7 @@
 #include "k_resident.cuh"
 #include "k_stream.cuh"
 #include "k_2d.cuh"
+#include "k_2d_fused.cuh"
 #include "k_stream_tb.cuh"
 
 using pbe::KParams;
@@ -71,6 +72,7 @@ struct pbe_ctx_s {
     int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
     bool temporal_block = false; // env PBE_TEMPORAL_BLOCK=1 enables NEXT-4 in k_stream (opt-in:
                                  // correct, but slower than plain streaming for batches so far)
+    bool unfused_2d = false;     // env PBE_2D_UNFUSED=1: two-sweep k_2d instead of k_2d_fused
 };
 
 static pbe_status fail(pbe_ctx ctx, pbe_status st, const char* fmt, ...) {
@@ -388,6 +390,70 @@ static pbe_status launch_2d(pbe_ctx ctx, KParams kp, int S, const double* f0, lo
 }
 
 // ------------------------------------------------------------------------------------
+// k_2d_fused launch (NEXT-1, default): both sweeps of a split step per HBM pass, warp strips
+// of 28 columns x 32 rows, 8 strips per tile/CTA; planes padded to whole tiles + ghost cells.
+// ------------------------------------------------------------------------------------
+static pbe_status launch_2d_fused(pbe_ctx ctx, KParams kp, int S, const double* f0, long long f0_stride,
+                                  double* f_final, cudaStream_t st) {
+    const pbe_config& cf = ctx->cfg;
+    const int N1 = cf.n_bins, N2 = cf.n_bins2;
+    const int NTX = (N1 + pbe::F2_TXC - 1) / pbe::F2_TXC, NTY = (N2 + pbe::F2_H - 1) / pbe::F2_H;
+    const long long P1 = (long long)NTX * pbe::F2_TXC + 8, R2 = (long long)NTY * pbe::F2_H + 4;
+    const int T2 = NTX * NTY;
+    const size_t smem = 0;
+    int sms = 0, per_sm = 0;
+    CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbe::k_2d_fused, pbe::F2_NT, smem));
+    if (per_sm < 1) return fail(ctx, PBE_ERR_CUDA, "k_2d_fused does not fit on an SM");
+    unsigned G = (unsigned)(per_sm * sms);
+    if ((long long)G > (long long)S * T2) G = (unsigned)((long long)S * T2);   // no idle CTAs
+    const size_t plane = (size_t)R2 * P1, buf = (size_t)S * plane;
+    CUDA_TRY(ctx, ctx->sbuf.ensure(2 * buf * sizeof(double)));
+    CUDA_TRY(ctx, ctx->spart.ensure(((size_t)S * T2 * 7 + (size_t)S * 8) * sizeof(double)));
+    CUDA_TRY(ctx, ctx->sbar.ensure(8 * sizeof(unsigned)));
+    CUDA_TRY(ctx, ctx->sfinal.ensure((size_t)2 * S * sizeof(int)));
+    CUDA_TRY(ctx, ctx->snscale.ensure((size_t)S * sizeof(unsigned long long)));
+    double* A = ctx->sbuf.as<double>();
+    double* B = A + buf;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbuf.p, 0, 2 * buf * sizeof(double), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbar.p, 0, 8 * sizeof(unsigned), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sfinal.p, 0, (size_t)2 * S * sizeof(int), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->snscale.p, 0, (size_t)S * sizeof(unsigned long long), st));
+    pbe::k_2d_fused_load<<<dim3(T2, S), 256, 0, st>>>(f0, f0_stride, N1, N2, A, P1, R2, NTX, ctx->spart.as<double>(),
+                                                      ctx->snscale.as<unsigned long long>(), cf.L_lo, cf.dL, cf.L2_lo,
+                                                      cf.dL2);
+    CUDA_TRY(ctx, cudaGetLastError());
+    pbe::Params2DF p{};
+    p.kp = kp;
+    p.N2 = N2; p.L2_lo = cf.L2_lo; p.dL2 = cf.dL2; p.inv_dL2 = 1.0 / cf.dL2;
+    p.A = A; p.B = B; p.P1 = P1; p.R2 = R2; p.NTX = NTX; p.NTY = NTY;
+    p.part = ctx->spart.as<double>();
+    p.bar = ctx->sbar.as<unsigned>();
+    p.nscale_bits = ctx->snscale.as<unsigned long long>();
+    p.final_buf = ctx->sfinal.as<int>();
+    p.cnt = reinterpret_cast<unsigned*>(ctx->sfinal.as<int>() + S);
+    p.tot = ctx->spart.as<double>() + (size_t)S * T2 * 7;
+    p.work = ctx->sbar.as<unsigned>() + 6;
+    void* args[] = {&p};
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)pbe::k_2d_fused, dim3(G), dim3(pbe::F2_NT), args, smem, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+    int launches = 2;
+    if (f_final) {
+        pbe::k_2d_fused_store<<<2 * sms, 256, 0, st>>>(A, B, p.final_buf, S, N1, N2, P1, R2, f_final);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
+    ctx->info.kernel = PBE_KERNEL_2D;
+    ctx->info.launches = launches;
+    ctx->info.threads_per_cta = pbe::F2_NT;
+    ctx->info.ctas = (int)G;
+    ctx->info.cluster = 1;
+    ctx->info.bins_per_thread = pbe::K2D_K;
+    return PBE_OK;
+}
+
+// ------------------------------------------------------------------------------------
 // C ABI
 // ------------------------------------------------------------------------------------
 extern "C" {
@@ -438,6 +504,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (const char* e = getenv("PBE_CLUSTER2")) ctx->cluster2 = atoi(e) != 0;
     if (const char* e = getenv("PBE_RESIDENT_K")) ctx->resident_k = atoi(e);
     if (const char* e = getenv("PBE_TEMPORAL_BLOCK")) ctx->temporal_block = atoi(e) != 0;
+    if (const char* e = getenv("PBE_2D_UNFUSED")) ctx->unfused_2d = atoi(e) != 0;
     ctx->device = device;
     const size_t S = c.max_sims, M = c.n_samples, P = c.n_tangents;
     cudaError_t ea = cudaSuccess;
@@ -616,7 +683,8 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     ctx->info = pbe_run_info{};
     ctx->info.steps_per_pass = 1;
     if (two_d) {
-        pbe_status r = launch_2d(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st);
+        pbe_status r = ctx->unfused_2d ? launch_2d(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st)
+                                       : launch_2d_fused(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st);
         if (r != PBE_OK) return r;
     } else if (kind == PBE_KERNEL_RESIDENT) {
         const int nt = ((N + rv->K - 1) / rv->K + 31) / 32 * 32;

@@ -62,7 +62,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libpbe.so")
+    # PBE_LIB: an alternative build of the same library (tools/build_variant.py A/B runs)
+    return os.environ.get("PBE_LIB") or os.path.join(_HERE, "libpbe.so")
 
 
 def load_library():

@@ -25,12 +25,21 @@
 
 namespace pbe {
 
+#ifndef PBE_F2_H
+#define PBE_F2_H 32
+#endif
+#ifndef PBE_F2_RB
+#define PBE_F2_RB 4
+#endif
+#ifndef PBE_F2_MINB
+#define PBE_F2_MINB 3
+#endif
 constexpr int F2_W = 28;                       // owned columns per warp strip
-constexpr int F2_H = 32;                       // owned rows per strip
+constexpr int F2_H = PBE_F2_H;                 // owned rows per strip
 constexpr int F2_WARPS = 8;                    // strips per tile (CTA)
 constexpr int F2_NT = 32 * F2_WARPS;
 constexpr int F2_TXC = F2_W * F2_WARPS;        // tile width (columns)
-constexpr int F2_RB = 4;                       // rows per load batch (loads in flight per lane)
+constexpr int F2_RB = PBE_F2_RB;               // rows per load batch (ping-pong prefetch)
 
 struct Params2DF {
     KParams kp;
@@ -50,90 +59,116 @@ struct Params2DF {
 };
 
 // Limited flux term kap psi(a, b) = k2 ab/(a+b) (0 unless ab > 0), k2 = |C|(1-|C|) = 2 kap
-// (psi = 2ab/(a+b) is the van Leer limited slope); upwind: 0.
-template <bool VL>
-__device__ __forceinline__ double limited(double a, double b, double k2) {
-    if (!VL) return 0.0;
-    const double ab = a * b;
-    return ab > 0.0 ? (k2 * ab) * rcp_nr(a + b) : 0.0;
+// (psi = 2ab/(a+b) is the van Leer limited slope), in the select-free
+// form psi = (a|b| + |a|b) / (|a| + |b|): the numerator is 2ab when ab > 0 and exactly 0
+// otherwise; the denominator is |a+b| when ab > 0 (+1e-300 keeps 0/0 out; it changes no
+// quotient with |a+b| > 1e-284).  Upwind passes k2 = 0 (exactly 0 term).
+__device__ __forceinline__ double limited(double a, double b, double k2h) {   // k2h = k2 / 2
+    const double num = fma(fabs(a), b, a * fabs(b));
+    const double den = (fabs(a) + fabs(b)) + 1e-300;
+    return (k2h * num) * rcp_nr(den);
 }
 
-// One warp strip: march rows j0-2 .. j0+H+1 of fin, write owned cells to fout.  Moments: per
-// lane sums over the strip's rows, S0 = sum v, S1 = sum v L2, S2 = sum v L2^2 (S2 every step,
-// S0/S1 on sample steps); the caller applies the column weights.
-template <bool VL, bool NEG1, bool NEG2>
+// Sliding state of one lane's column for sweep 2.
+struct ColState {
+    double gm3, gm2, gm1, Fprev;     // g of rows r-3, r-2, r-1; face below row r-3
+    double S0, S1, S2;               // sum v, sum v L2, sum v L2^2 over emitted rows
+    double L2;                       // L2 centre of the next emitted row
+    bool bad;
+};
+
+// One input row of a strip: sweep 1 across lanes, then the sweep-2 face between rows r-2 and
+// r-1; if EMIT, the finished cell of row r-2 is clipped, stored and added to the moments.
+template <bool NEG1, bool NEG2, bool EMIT>
+__device__ __forceinline__ void strip_row(double w, ColState& cs, double C1, double k1, double C2, double k2,
+                                          double clip, double dL2, bool own, bool ok, bool sample, double* dst) {
+    const double wm1 = __shfl_up_sync(0xffffffffu, w, 1);
+    double F;
+    if (!NEG1) {
+        const double wm2 = __shfl_up_sync(0xffffffffu, w, 2);
+        F = fma(C1, wm1, limited(wm1 - wm2, w - wm1, k1));
+    } else {
+        const double wp1 = __shfl_down_sync(0xffffffffu, w, 1);
+        F = fma(C1, w, limited(wp1 - w, w - wm1, k1));
+    }
+    const double Fp = __shfl_down_sync(0xffffffffu, F, 1);
+    const double g = w - (Fp - F);                 // ghost rows: w = 0 in all lanes -> g = 0
+    double F2;
+    if (!NEG2) F2 = fma(C2, cs.gm2, limited(cs.gm2 - cs.gm3, cs.gm1 - cs.gm2, k2));
+    else       F2 = fma(C2, cs.gm1, limited(g - cs.gm1, cs.gm1 - cs.gm2, k2));
+    if (EMIT) {                                    // ok: row r-2 < N2 (no branch: keeps the warp converged)
+        const bool keep = own && ok;
+        double v = cs.gm2 - (F2 - cs.Fprev);
+        cs.bad |= keep && v < -clip;               // status NEG; the stored state is then moot
+        v = keep ? fmax(v, 0.0) : 0.0;             // round-off clip (R-17); dropped cells add nothing
+        if (keep) *dst = v;
+        const double vl2 = v * cs.L2;
+        cs.S2 = fma(vl2, cs.L2, cs.S2);            // mu12 every step
+        cs.S0 += v; cs.S1 += vl2;                  // used on sample steps only
+        cs.L2 += dL2;
+    }
+    cs.Fprev = F2;
+    cs.gm3 = cs.gm2; cs.gm2 = cs.gm1; cs.gm1 = g;
+}
+
+// One warp strip: march rows j0-2 .. j0+H+1 of fin (RB-row load batches, ping-pong prefetch),
+// write the owned cells of rows j0 .. j0+H-1 to fout.  Per-lane moment sums in cs (the caller
+// applies the column weights and drops the halo lanes).
+template <bool NEG1, bool NEG2>
 __device__ __forceinline__ void strip_march(const double* __restrict__ fin, double* __restrict__ fout, long long P1,
                                             int N1, int N2, int is, int j0, double C1, double k1, double C2, double k2,
-                                            double clip, bool sample, double dL2, double L2_lo, double (&S)[3],
-                                            bool& bad) {
+                                            double clip, bool sample, double dL2, double L2_lo, ColState& cs) {
+    constexpr int RB = F2_RB, NB = (F2_H + 4) / F2_RB;
+    static_assert((F2_H + 4) % F2_RB == 0 && NB % 2 == 1 && RB >= 4, "batch layout");
     const int lane = threadIdx.x & 31;
     const int i = is - 2 + lane;
     const bool own = lane >= 2 && lane < 2 + F2_W && i < N1;
     const double* src = fin + (size_t)j0 * P1 + (is + lane);       // padded row j0 = real row j0-2
     double* dst = fout + (size_t)(j0 + 2) * P1 + (is + lane);      // padded row of real row j0
-    double gm3 = 0.0, gm2 = 0.0, gm1 = 0.0, Fprev = 0.0;
-    constexpr int NR = F2_H + 4;
-    static_assert(NR % F2_RB == 0, "row batches");
-    const int rlo = 2 - j0, rhi = N2 + 2 - j0;                     // rr in [rlo, rhi): real row
-    const int jend = (N2 - j0 < F2_H ? N2 - j0 : F2_H) + 4;        // emit while rr < jend
-    double L2 = fma((double)j0, dL2, L2_lo + 0.5 * dL2);           // centre of the next emitted row
-    double wb[F2_RB];
+    const int nrow = N2 - j0;                                      // emitted rows < nrow
+    cs.gm3 = cs.gm2 = cs.gm1 = cs.Fprev = 0.0;
+    cs.L2 = fma((double)j0, dL2, L2_lo + 0.5 * dL2);
+    double A[RB], B[RB];
 #pragma unroll
-    for (int q = 0; q < F2_RB; ++q) wb[q] = src[(size_t)q * P1];
-    src += F2_RB * P1;
+    for (int q = 0; q < RB; ++q) A[q] = src[(size_t)q * P1];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) B[q] = src[(size_t)(RB + q) * P1];
+    // batch 0: rows 0..3 fill the window, rows 4..RB-1 emit rows j0 .. j0+RB-5
+#pragma unroll
+    for (int q = 0; q < 4; ++q) strip_row<NEG1, NEG2, false>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, true, sample, dst);
+#pragma unroll
+    for (int q = 4; q < RB; ++q) {
+        strip_row<NEG1, NEG2, true>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, q - 4 < nrow, sample, dst);
+        dst += P1;
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) A[q] = src[(size_t)(2 * RB + q) * P1];
+    int e = RB - 4;                                                // emitted rows so far
 #pragma unroll 1
-    for (int rb = 0; rb < NR; rb += F2_RB) {
-        double wn[F2_RB];
-        const bool more = rb + F2_RB < NR;
-        if (more) {
+    for (int k = 1; k < NB; k += 2) {
 #pragma unroll
-            for (int q = 0; q < F2_RB; ++q) wn[q] = src[(size_t)q * P1];
-            src += F2_RB * P1;
+        for (int q = 0; q < RB; ++q) {
+            strip_row<NEG1, NEG2, true>(B[q], cs, C1, k1, C2, k2, clip, dL2, own, e + q < nrow, sample, dst);
+            dst += P1;
+        }
+        if (k + 2 < NB) {
+#pragma unroll
+            for (int q = 0; q < RB; ++q) B[q] = src[(size_t)((k + 2) * RB + q) * P1];
         }
 #pragma unroll
-        for (int q = 0; q < F2_RB; ++q) {
-            const int rr = rb + q;
-            const double w = wb[q];
-            // ---- sweep 1 along the row (lanes = columns) ----
-            const double wm1 = __shfl_up_sync(0xffffffffu, w, 1);
-            double F;
-            if (!NEG1) {
-                const double wm2 = __shfl_up_sync(0xffffffffu, w, 2);
-                F = fma(C1, wm1, limited<VL>(wm1 - wm2, w - wm1, k1));
-            } else {
-                const double wp1 = __shfl_down_sync(0xffffffffu, w, 1);
-                F = fma(C1, w, limited<VL>(wp1 - w, w - wm1, k1));
-            }
-            const double Fp = __shfl_down_sync(0xffffffffu, F, 1);
-            double g = w - (Fp - F);
-            if (rr < rlo || rr >= rhi) g = 0.0;                     // ghost rows of sweep 2
-            // ---- sweep 2 down the column: face between rows r-2 and r-1 ----
-            double F2;
-            if (!NEG2) F2 = fma(C2, gm2, limited<VL>(gm2 - gm3, gm1 - gm2, k2));
-            else       F2 = fma(C2, gm1, limited<VL>(g - gm1, gm1 - gm2, k2));
-            if (rr >= 4 && rr < jend) {                             // emit row r-2 (j0 .. min(j0+H, N2)-1)
-                double v = gm2 - (F2 - Fprev);
-                if (own) {
-                    if (v < 0.0) { if (v >= -clip) v = 0.0; else bad = true; }   // round-off clip (R-17)
-                    *dst = v;
-                    const double vl2 = v * L2;
-                    S[2] = fma(vl2, L2, S[2]);                      // mu12 every step
-                    if (sample) { S[0] += v; S[1] += vl2; }
-                }
-                dst += P1;
-                L2 += dL2;
-            }
-            Fprev = F2;
-            gm3 = gm2; gm2 = gm1; gm1 = g;
+        for (int q = 0; q < RB; ++q) {
+            strip_row<NEG1, NEG2, true>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, e + RB + q < nrow, sample, dst);
+            dst += P1;
         }
-        if (more) {
+        if (k + 3 < NB) {
 #pragma unroll
-            for (int q = 0; q < F2_RB; ++q) wb[q] = wn[q];
+            for (int q = 0; q < RB; ++q) A[q] = src[(size_t)((k + 3) * RB + q) * P1];
         }
+        e += 2 * RB;
     }
 }
 
-__global__ void __launch_bounds__(F2_NT, 3) k_2d_fused(const Params2DF p) {
+__global__ void __launch_bounds__(F2_NT, PBE_F2_MINB) k_2d_fused(const Params2DF p) {
     const KParams& kp = p.kp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = F2_WARPS;
@@ -239,27 +274,28 @@ __global__ void __launch_bounds__(F2_NT, 3) k_2d_fused(const Params2DF p) {
             const int is = tx * F2_TXC + warp * F2_W, j0 = ty * F2_H;
             double acc[6] = {0, 0, 0, 0, 0, 0};
             bool bad = false;
-            if (is < N1) {                                           // warp-uniform
+            {   // strips past N1 march the zero padding (inside P1) and emit nothing
                 const double C1 = s_C1[s], k1 = s_k1[s], C2 = s_C2[s], k2 = s_k2[s];
                 const double clip = s_ss[s].clip;
                 const bool sample = s_sample[s] != 0;
                 const double* fi = fin + (size_t)s * PL;
                 double* fo = fout + (size_t)s * PL;
-                double Sm[3] = {0.0, 0.0, 0.0};
-                const int sel = (vl ? 4 : 0) + (C1 < 0.0 ? 2 : 0) + (C2 < 0.0 ? 1 : 0);
-#define PBE_STRIP(V, A, B) strip_march<V, A, B>(fi, fo, P1, N1, N2, is, j0, C1, k1, C2, k2, clip, sample, p.dL2, \
-                                                p.L2_lo, Sm, bad)
+                ColState cs;
+                cs.S0 = cs.S1 = cs.S2 = 0.0;
+                cs.bad = false;
+                const double k1v = vl ? 0.5 * k1 : 0.0, k2v = vl ? 0.5 * k2 : 0.0;   // k2/2; upwind: no limited term
+                const int sel = (C1 < 0.0 ? 2 : 0) + (C2 < 0.0 ? 1 : 0);
+#define PBE_STRIP(A, B) strip_march<A, B>(fi, fo, P1, N1, N2, is, j0, C1, k1v, C2, k2v, clip, sample, p.dL2, p.L2_lo, cs)
                 switch (sel) {
-                    case 0: PBE_STRIP(false, false, false); break;
-                    case 1: PBE_STRIP(false, false, true); break;
-                    case 2: PBE_STRIP(false, true, false); break;
-                    case 3: PBE_STRIP(false, true, true); break;
-                    case 4: PBE_STRIP(true, false, false); break;
-                    case 5: PBE_STRIP(true, false, true); break;
-                    case 6: PBE_STRIP(true, true, false); break;
-                    default: PBE_STRIP(true, true, true); break;
+                    case 0: PBE_STRIP(false, false); break;
+                    case 1: PBE_STRIP(false, true); break;
+                    case 2: PBE_STRIP(true, false); break;
+                    default: PBE_STRIP(true, true); break;
                 }
 #undef PBE_STRIP
+                bad = cs.bad;
+                const bool own = lane >= 2 && lane < 2 + F2_W && is - 2 + lane < N1;
+                const double Sm[3] = {own ? cs.S0 : 0.0, own ? cs.S1 : 0.0, own ? cs.S2 : 0.0};
                 // column weights: mu_pq = dL1 dL2 sum L1^p L2^q n
                 const double L1 = fma((double)(is - 2 + lane), kp.dL, kp.L_lo + 0.5 * kp.dL);
                 acc[5] = L1 * (wa * Sm[2]);

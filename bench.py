@@ -307,11 +307,15 @@ def main():
     def roofline(w, info, bu_local, kms, workload):
         P = w.n_tangents
         if info["kernel"] in (pb.KERNEL_STREAM, pb.KERNEL_2D):
-            bytes_per = 16.0 * (1 + P) * (2.0 if info["kernel"] == pb.KERNEL_2D else 1.0)   # 2D: two sweeps
+            # 2D: the fused kernel reads + writes each cell once per split step (16 B); the unfused
+            # one (PBE_2D_UNFUSED=1) does that once per sweep (32 B)
+            unfused = info["kernel"] == pb.KERNEL_2D and os.environ.get("PBE_2D_UNFUSED", "0") not in ("", "0")
+            bytes_per = 16.0 * (1 + P) * (2.0 if unfused else 1.0)
             achieved = bytes_per * bu_local / (kms * 1e-3) / 1e9
             hbm = float(peaks.get("hbm_gbs", 6650.0))
+            kname = ("k_2d" if unfused else "k_2d_fused") if info["kernel"] == pb.KERNEL_2D else "k_stream"
             r = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm, traffic=None,
-                     kernel="k_2d" if info["kernel"] == pb.KERNEL_2D else "k_stream", bytes_per_bin_update=bytes_per,
+                     kernel=kname, bytes_per_bin_update=bytes_per,
                      peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s", kernel_ms=kms)
         else:
             f = flops_per_bin_update(w.limiter, P)

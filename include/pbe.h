@@ -66,12 +66,14 @@ enum {
     PBE_LAW_POLY = 2           /* theta = (a1..ak): sum_j a_j (S-1)^j for S > 1, else 0    */
 };
 enum { PBE_SOL_EXP = 0 /* (a, b): a exp(bT) */, PBE_SOL_POLY = 1 /* (s0,s1,s2) (R-13) */ };
+enum { PBE_MAX_PARAMS = 4096 };  /* kinetic parameters per simulation (POLY terms) */
 enum {
     PBE_KERNEL_AUTO = 0,      /* choose by N and lanes              */
     PBE_KERNEL_RESIDENT = 1,  /* one CTA per sim, state in registers across all steps     */
     PBE_KERNEL_CLUSTER = 2,   /* thread-block cluster per sim, DSMEM halo + reduction     */
     PBE_KERNEL_STREAM = 3,    /* grid-wide persistent kernel, HBM streaming, grid barrier */
-    PBE_KERNEL_2D = 4         /* 2D model (set by n_bins2 > 0): grid-wide split-sweep kernel */
+    PBE_KERNEL_2D = 4,        /* 2D model (set by n_bins2 > 0): grid-wide split-sweep kernel */
+    PBE_KERNEL_ADJOINT = 5    /* reported by pbe_last_run_info after pbe_run_adjoint (NEXT-3) */
 };
 
 typedef struct {
@@ -117,7 +119,9 @@ void pbe_destroy(pbe_ctx ctx);
 const char* pbe_last_error(pbe_ctx ctx);
 
 /* Kinetics of the next runs (row a1).
- *   theta        host [n_sims][n_params]   per-simulation kinetic parameters
+ *   theta        host [n_sims][n_params]   per-simulation kinetic parameters; n_params is 1
+ *                (CONST), 3 or 6 (ARRHENIUS_GD), 1..PBE_MAX_PARAMS (POLY: the paper grows
+ *                the polynomial to scale the parameter count, L565-572, L599)
  *   sol_params   host [n_sol]              solubility parameters (shared)
  *   knot_t       host [n_knots]            temperature-profile times (strictly increasing)
  *   knot_T       host [n_knots] or [n_sims][n_knots] (knot_T_per_sim = 0 / 1); T(t) is
@@ -160,6 +164,29 @@ pbe_status pbe_moments(pbe_ctx ctx, double* moments, int32_t* sim_status, int64_
  *   tangents  [n_sims][M][n_tangents][5] = d(c, mu0, mu1, mu2, mu3)/d(seed direction)
  *   grad      [n_sims][n_tangents] = d loss / d(seed direction), or NULL */
 pbe_status pbe_tangents(pbe_ctx ctx, double* tangents, double* grad, int32_t on_device);
+
+/* Reverse-mode gradient (NEXT-3; jax.grad with checkpointing, "for
+ * 1000 parameters specifically, jax-AD is 40x faster than jax-ND"): d loss / d theta for ALL
+ * n_params kinetic parameters of every simulation at the cost of about four primal marches,
+ * independent of n_params (tangent lanes cost one lane per direction).  The discrete adjoint
+ * of exactly the march pbe_run_batch performs: same steps, same branch decisions (sample
+ * landing, dt cap, clip), derivatives equal to pbe_tangents' up to rounding.
+ *   n0, n0_stride, n0_on_device, c0, t_samples: as pbe_run_batch
+ *   target            host [n_sims][n_samples][2] (required: the loss R-23 is differentiated)
+ *   checkpoint_every  store the distribution every K steps (0: K = ceil(sqrt(max_steps)));
+ *                     device memory per simulation = 8 B x (16 max_steps
+ *                     + N ceil(max_steps / K) + N (K + 1)) -- max_steps bounds the trace
+ * Restrictions (PBE_ERR_ARG): 1D model, sample mode (n_steps = 0), N <= 6144, n_params <=
+ * 16 x the CTA size.  The gradient is w.r.t. theta only (not the solubility parameters).
+ * Records, status, steps and loss of the forward pass are read with pbe_moments. */
+pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride,
+                           int32_t n0_on_device, const double* c0, const double* t_samples,
+                           const double* target, int32_t checkpoint_every, void* cuda_stream);
+
+/* Result of the last pbe_run_adjoint (synchronizes its stream):
+ *   grad  [n_sims][n_params] d loss / d theta (NaN for a simulation whose march failed)
+ *   loss  [n_sims] or NULL */
+pbe_status pbe_adjoint_gradient(pbe_ctx ctx, double* grad, double* loss, int32_t on_device);
 
 /* Introspection for tests and the benchmark harness. */
 typedef struct {

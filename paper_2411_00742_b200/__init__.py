@@ -26,12 +26,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIM_UPWIND, LIM_VANLEER = 0, 1
 LAW_CONST, LAW_ARRHENIUS_GD, LAW_POLY = 0, 1, 2
 SOL_EXP, SOL_POLY = 0, 1
-KERNEL_AUTO, KERNEL_RESIDENT, KERNEL_CLUSTER, KERNEL_STREAM, KERNEL_2D = 0, 1, 2, 3, 4
+KERNEL_AUTO, KERNEL_RESIDENT, KERNEL_CLUSTER, KERNEL_STREAM, KERNEL_2D, KERNEL_ADJOINT = 0, 1, 2, 3, 4, 5
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_CFL", 3: "ERR_NEGATIVE", 4: "ERR_INFEASIBLE",
           5: "ERR_MAXSTEPS", 6: "ERR_CUDA", 7: "ERR_NOMEM", 8: "ERR_STATE"}
 
 # every symbol include/pbe.h declares
-EXPORTS = ("pbe_create", "pbe_destroy", "pbe_last_error", "pbe_set_kinetics", "pbe_run_batch",
+EXPORTS = ("pbe_create", "pbe_destroy", "pbe_last_error", "pbe_set_kinetics", "pbe_run_batch", "pbe_run_adjoint",
+           "pbe_adjoint_gradient",
            "pbe_moments", "pbe_tangents", "pbe_last_run_info", "pbe_version")
 
 
@@ -91,6 +92,10 @@ def load_library():
     lib.pbe_moments.restype = C.c_int
     lib.pbe_tangents.argtypes = [vp, vp, vp, C.c_int32]
     lib.pbe_tangents.restype = C.c_int
+    lib.pbe_run_adjoint.argtypes = [vp, C.c_int32, vp, C.c_int64, C.c_int32, vp, vp, vp, C.c_int32, vp]
+    lib.pbe_run_adjoint.restype = C.c_int
+    lib.pbe_adjoint_gradient.argtypes = [vp, vp, vp, C.c_int32]
+    lib.pbe_adjoint_gradient.restype = C.c_int
     lib.pbe_last_run_info.argtypes = [vp, C.POINTER(RunInfo)]
     lib.pbe_last_run_info.restype = C.c_int
     lib.pbe_version.argtypes = []
@@ -185,6 +190,36 @@ class Context:
         self._keep = [n0, c0, ts, tg]
         self._check(self._lib.pbe_run_batch(self._h, self.n_sims, _ptr(n0), stride, 1 if on_dev else 0, _ptr(c0),
                                             _ptr(ts), _ptr(tg), _ptr(n_final), _ptr(ndot_final), sp))
+
+    def run_adjoint(self, n0, c0, t_samples, target, checkpoint_every: int = 0, stream=None):
+        """NEXT-3: forward march + discrete adjoint (pbe_run_adjoint); read the result with
+        adjoint_gradient() and the forward records with moments()."""
+        on_dev = not isinstance(n0, np.ndarray)
+        if not on_dev:
+            n0 = _host(n0)
+        rows = n0.shape[0] if n0.ndim == 2 else 1
+        stride = 0 if rows == 1 else self.cfg.n_bins
+        c0 = _host(np.atleast_1d(c0)); ts = _host(t_samples); tg = _host(target)
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.device) if torch.cuda.is_available() else None
+        sp = None if stream is None else C.c_void_p(stream.cuda_stream)
+        self._keep = [n0, c0, ts, tg]
+        self._check(self._lib.pbe_run_adjoint(self._h, self.n_sims, _ptr(n0), stride, 1 if on_dev else 0, _ptr(c0),
+                                              _ptr(ts), _ptr(tg), int(checkpoint_every), sp))
+
+    def adjoint_gradient(self, n_params: int, on_device: bool = False):
+        """d loss / d theta [S][n_params] and loss [S] of the last run_adjoint."""
+        S = self.n_sims
+        if on_device:
+            import torch
+            dev = torch.device("cuda", self.device)
+            out = dict(grad=torch.empty((S, n_params), dtype=torch.float64, device=dev),
+                       loss=torch.empty(S, dtype=torch.float64, device=dev))
+        else:
+            out = dict(grad=np.empty((S, n_params)), loss=np.empty(S))
+        self._check(self._lib.pbe_adjoint_gradient(self._h, _ptr(out["grad"]), _ptr(out["loss"]), 1 if on_device else 0))
+        return out
 
     def moments(self, on_device: bool = False, out: Optional[dict] = None):
         """Records of the last run.  `out` may supply preallocated destinations (e.g. pinned

@@ -1,0 +1,460 @@
+// =====================================================================================
+//  k_adjoint — NEXT-3: reverse-mode (discrete adjoint) gradient of the RSS loss with
+//  respect to every kinetic parameter, with trajectory checkpointing.  This is the regime
+//  the paper reaches with jax.grad + checkpointing ("for
+//  1000 parameters specifically, jax-AD is 40x faster than jax-ND").  The cost of one
+//  gradient is a fixed number of passes over the march, independent of the parameter count.
+//
+//  Step k of the forward march (the same discrete map as the other kernels; rows a1-a7):
+//     G^k   = law(S(c^k, T(t^k)); theta)                       (row a1)
+//     C^k, dt^k, landing = time_step(G^k, t^k)                 (row a2, R-7..R-9)
+//     n^{k+1} = Phi(n^k; C^k)  (flux form, clip R-17)          (rows a3, a4)
+//     c^{k+1} = c^k - rho_c k_v (mu3(n^{k+1}) - mu3p^k),  mu3p^{k+1} = mu3(n^{k+1})
+//     t^{k+1} = landing ? t_m : t^k + dt^k
+//     loss   += ((c - c^)/rms_c)^2 + ((mu1/mu0 - L^)/rms_L)^2 at samples  (row a7, R-23)
+//  theta enters ONLY through the scalar G^k, so
+//     dL/dtheta_j = sum_k lambda_G^k dG^k/dtheta_j
+//  with lambda_G^k the adjoint of G^k.  The vector part is the transposed flux update
+//     Lambda_f = lambda_f - lambda_{f-1}   (face f between bins f-1 and f)
+//     lambda^k_j = lambda^{k+1}_j + sum_{faces f touching j} Lambda_f dF_f/dn_j
+//     lambda_C^k = sum_f Lambda_f dF_f/dC,     dF/dC = n_up + beta psi  (kapdot = beta Cdot)
+//  using the same face partials as the tangent lanes (k_resident.cuh: w_lo, w_mid, w_hi, g).
+//  The scalar chain (c, t, G) -> (C, t') is linearised once in the forward pass with 3 lanes of
+//  dual numbers (seeds dc, dt, dG) and stored in a per-step trace; the reverse pass only needs
+//  that trace, the face partials at n^k and the clip marks of n^{k+1}.
+//
+//  Checkpointing: the forward pass stores n^k every Kseg steps; the reverse pass walks the
+//  segments backwards, re-marches each one from its checkpoint (kinetics not re-evaluated: C^k
+//  comes from the trace, so the recomputed states are bitwise the forward ones) into a segment
+//  buffer, then runs the adjoint steps of the segment.  Memory per simulation: trace
+//  16 doubles x steps, checkpoints N x steps/Kseg, segment N x (Kseg + 1).
+//
+//  Clip marks: a bin zeroed by the round-off clip (R-17) is stored as -0.0 (an exact zero for
+//  all arithmetic); every other zero is canonicalised to +0.0.  The adjoint of a clipped bin is
+//  0, exactly as the tangent lanes zero a clipped bin's tangents.
+//
+//  One CTA per simulation, K bins per thread (contiguous), state and adjoint in shared memory
+//  double-buffered by step parity; warp 0 runs the scalar phases (two barriers per step).
+// =====================================================================================
+#pragma once
+#include "pbe_device.cuh"
+
+namespace pbe {
+
+constexpr int ADJ_TR = 16;        // doubles per step in the scalar trace
+constexpr int ADJ_GMAX = 16;      // dL/dtheta accumulators per thread
+enum AdjTrace {
+    TR_C = 0, TR_KAP2, TR_BETA2,          // Courant number, 2 kap, 2 beta (kapdot = beta Cdot)
+    TR_CC, TR_CT, TR_CG,                  // dC/dc, dC/dt (total, through G), dC/dG
+    TR_TC, TR_TT, TR_TG,                  // dt'/dc, dt'/dt, dt'/dG   (t' = t^{k+1})
+    TR_S, TR_T,                           // supersaturation and temperature of the step
+    TR_LC, TR_L0, TR_L1                   // d loss / d(c, mu0, mu1)(n^{k+1}) if step k lands on a sample
+};
+
+struct AdjParams {
+    KParams kp;           // 1D, P = 0, sample mode, target set
+    double* ck;           // [S][n_ck][N] checkpoints n^{j Kseg}
+    double* seg;          // [S][Kseg + 1][N] states n^{k0} .. n^{k1} of the current segment
+    double* tr;           // [S][max_steps][ADJ_TR]
+    double* gtheta;       // [S][n_params]
+    long long n_ck;       // checkpoint slots per simulation
+    int Kseg;
+};
+
+// dG/dtheta_j at (S, T) in closed form (the parameters enter the laws of growth_rate as
+// below; dpow(x, y) = exp(y log x) there).
+__device__ __forceinline__ double dG_dtheta(const KParams& kp, const double* __restrict__ th, double S, double T, int j) {
+    if (kp.law == LAW_CONST) return j == 0 ? 1.0 : 0.0;
+    if (kp.law == LAW_ARRH) {
+        const double Tk = T + 273.15;
+        if (S > 1.0) {
+            if (j > 2) return 0.0;
+            const double lx = log(S - 1.0);
+            const double EP = exp(-th[1] / Tk) * exp(th[2] * lx);
+            return j == 0 ? EP : (j == 1 ? -th[0] * EP / Tk : th[0] * EP * lx);
+        }
+        if (S < 1.0 && kp.n_params >= 6) {
+            if (j < 3) return 0.0;
+            const double lx = log(1.0 - S);
+            const double EP = exp(-th[4] / Tk) * exp(th[5] * lx);
+            return j == 3 ? -EP : (j == 4 ? th[3] * EP / Tk : -th[3] * EP * lx);
+        }
+        return 0.0;
+    }
+    if (S > 1.0) return pow(S - 1.0, (double)(j + 1));           // POLY: G = sum_j a_j (S-1)^(j+1)
+    return 0.0;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
+    const KParams& kp = ap.kp;
+    const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int NT = blockDim.x, NW = NT >> 5;
+    const int N = kp.N, NP = NT * K + 4;
+    const int i0 = tid * K;
+    const bool vl = kp.limiter == LIM_VANLEER;
+    const double rho = kp.rho_kv;
+    const int Kseg = ap.Kseg;
+    double* trs = ap.tr + (size_t)s * kp.max_steps * ADJ_TR;
+    double* cks = ap.ck + (size_t)s * ap.n_ck * N;
+    double* sgs = ap.seg + (size_t)s * (Kseg + 1) * N;
+
+    extern __shared__ double sm[];
+    double* nb = sm;                      // [2][NP] states, bin i at [i + 2]
+    double* lb = sm + 2 * NP;             // [2][NP] adjoints
+    __shared__ double s_red[32][4];
+    __shared__ double s_sc[12];
+    __shared__ int s_go, s_sample, s_bad, s_ok;
+    __shared__ long long s_nsteps;
+    enum { SC_C = 0, SC_KAP2, SC_BETA2, SC_LM, SC_L0, SC_L1, SC_LG, SC_S, SC_T, SC_CLIP };
+
+    for (int j = tid; j < 4 * NP; j += NT) sm[j] = 0.0;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    double lmax = 0.0;
+    {
+        const double* n0 = kp.n0 + (size_t)s * kp.n0_stride;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = i0 + k;
+            if (i < N) { const double v = n0[i]; nb[i + 2] = v; lmax = fmax(lmax, v); }
+        }
+    }
+    // block sums of mu0..mu3 of nb[q] (all four if `all`, else mu3) -> s_red totals in warp 0
+    auto moment_partials = [&](int q, bool all) {
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* x = nb + q * NP + 2;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = i0 + k;
+            if (i < N) {
+                const double L = fma((double)i, kp.dL, kp.L_lo + 0.5 * kp.dL);
+                const double w0 = kp.dL * x[i], w1 = w0 * L, w2 = w1 * L;
+                a[3] = fma(w2, L, a[3]);
+                if (all) { a[0] += w0; a[1] += w1; a[2] += w2; }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) a[m] += __shfl_xor_sync(0xffffffffu, a[m], off);
+        if (lane == 0)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) s_red[warp][m] = a[m];
+    };
+    auto block_total = [&](int m) -> double {                      // warp 0, after a barrier
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += s_red[w][m];
+        return t;
+    };
+    // forward update nb[q] -> nb[q^1] (eq-highRes_growth, flux form; clip marks as -0.0)
+    auto update = [&](int q, double C, double kap2, double clip) -> bool {
+        const double* in = nb + q * NP + i0;                       // in[j] = bin i0 - 2 + j
+        double* out = nb + (q ^ 1) * NP + i0 + 2;
+        double w[K + 4], F[K + 1];
+#pragma unroll
+        for (int j = 0; j < K + 4; ++j) w[j] = in[j];
+#pragma unroll
+        for (int f = 0; f <= K; ++f) {                             // face between bins i0+f-1 | i0+f
+            if (C >= 0.0) {
+                const double h = vl ? 0.5 * psi_vl(w[f + 1] - w[f], w[f + 2] - w[f + 1]) : 0.0;
+                F[f] = fma(C, w[f + 1], kap2 * h);
+            } else {
+                const double h = vl ? 0.5 * psi_vl(w[f + 3] - w[f + 2], w[f + 2] - w[f + 1]) : 0.0;
+                F[f] = fma(C, w[f + 2], kap2 * h);
+            }
+        }
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (i0 + k < N) {
+                double v = (w[k + 2] - (F[k + 1] - F[k])) + 0.0;     // +0.0: canonical zero
+                if (v < 0.0) { if (v >= -clip) v = -0.0; else bad = true; }   // R-17 (mark)
+                out[k] = v;
+            }
+        }
+        return bad;
+    };
+
+    moment_partials(0, false);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
+    if (lane == 0) s_red[warp][0] = lmax;          // mu0 slot reused for max(n0) (mu3 in slot 3)
+    __syncthreads();
+
+    // ---- warp-0 scalar state of the forward pass ----------------------------------------------
+    const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, -1, kp.n_params, kp.n_params + kp.n_sol};
+    const double* kT = kp.knot_T + (size_t)s * kp.knotT_stride;
+    const double* tgt = kp.target + (size_t)s * kp.M * 2;
+    double c = kp.c0[s], t = 0.0, mu3p = 0.0, loss = 0.0, rms_c = 1.0, rms_L = 1.0, dt = 0.0;
+    long long nstep = 0;
+    int m = 0, status = ST_OK;
+    bool landing = false;
+    // kinetics of the step from (c, t) + its linearisation (lane 0: dc, lane 1: dt, lane 2: dG)
+    auto kinetics = [&](long long k) -> bool {
+        const KinCache KC = kin_cache(kp, KL, kT);
+        const D1 cD = mk(c, lane == 0 ? 1.0 : 0.0), tD = mk(t, lane == 1 ? 1.0 : 0.0);
+        D1 T;
+        const D1 S = supersaturation(kp, KL, kT, KC, tD, cD, T);
+        D1 G = growth_rate(kp, KL, S, T);
+        if (lane == 2) G = mk(G.v, 1.0);
+        const double tn = kp.t_samples[m];
+        const StepScalars sc = time_step(kp, G, tD, tn, false);
+        if (sc.err != ST_OK) { status = sc.err; return false; }
+        const D1 tp = sc.landing ? mk(tn) : tD + sc.dt;
+        const double Cv = sc.C.v;
+        const double beta = Cv > 0.0 ? 0.5 * (1.0 - 2.0 * Cv) : (Cv < 0.0 ? -0.5 * (1.0 + 2.0 * Cv) : 0.0);
+        const double dC0 = __shfl_sync(0xffffffffu, sc.C.d, 0), dC1 = __shfl_sync(0xffffffffu, sc.C.d, 1);
+        const double dC2 = __shfl_sync(0xffffffffu, sc.C.d, 2);
+        const double dT0 = __shfl_sync(0xffffffffu, tp.d, 0), dT1 = __shfl_sync(0xffffffffu, tp.d, 1);
+        const double dT2 = __shfl_sync(0xffffffffu, tp.d, 2);
+        if (lane == 0) {
+            double* r = trs + (size_t)k * ADJ_TR;
+            r[TR_C] = Cv; r[TR_KAP2] = 2.0 * sc.kap.v; r[TR_BETA2] = 2.0 * beta;
+            r[TR_CC] = dC0; r[TR_CT] = dC1; r[TR_CG] = dC2;
+            r[TR_TC] = dT0; r[TR_TT] = dT1; r[TR_TG] = dT2;
+            r[TR_S] = S.v; r[TR_T] = T.v;
+            r[TR_LC] = 0.0; r[TR_L0] = 0.0; r[TR_L1] = 0.0;
+            s_sc[SC_C] = Cv; s_sc[SC_KAP2] = 2.0 * sc.kap.v;
+        }
+        dt = sc.dt.v;
+        landing = sc.landing;
+        return true;
+    };
+    if (warp == 0) {
+        double nmax = 0.0;
+        for (int w = 0; w < NW; ++w) nmax = fmax(nmax, s_red[w][0]);
+        mu3p = block_total(3);
+        double sc2 = 0.0, sl2 = 0.0;
+        for (int j = lane; j < kp.M; j += 32) { sc2 += tgt[2 * j] * tgt[2 * j]; sl2 += tgt[2 * j + 1] * tgt[2 * j + 1]; }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            sc2 += __shfl_xor_sync(0xffffffffu, sc2, off);
+            sl2 += __shfl_xor_sync(0xffffffffu, sl2, off);
+        }
+        rms_c = sqrt(sc2 / kp.M); rms_L = sqrt(sl2 / kp.M);
+        bool go = kp.max_steps > 0;
+        if (!go) status = ST_MAXSTEPS;
+        if (go) go = kinetics(0);
+        if (lane == 0) {
+            s_go = go;
+            s_sample = go && landing;
+            s_sc[SC_CLIP] = 1e-12 * nmax;
+        }
+    }
+    __syncthreads();
+    const double clip = s_sc[SC_CLIP];
+
+    // ---- forward pass: checkpoints + trace -------------------------------------------------------
+    int q = 0;
+    long long k = 0;
+    while (s_go) {
+        if (k % Kseg == 0) {
+            double* ckp = cks + (size_t)(k / Kseg) * N;
+#pragma unroll
+            for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + i0 + j + 2];
+        }
+        if (update(q, s_sc[SC_C], s_sc[SC_KAP2], clip)) s_bad = 1;
+        moment_partials(q ^ 1, s_sample != 0);
+        __syncthreads();
+        if (warp == 0) {
+            const bool sample = s_sample != 0;
+            const double mu3 = block_total(3);
+            const double cn = c - rho * (mu3 - mu3p);                     // eq-discrete_mass_balance
+            bool go = true;
+            if (s_bad) { status = ST_NEG; go = false; }
+            else if (cn < 0.0) { status = ST_INFEAS; go = false; }
+            else {
+                c = cn; mu3p = mu3;
+                t = landing ? kp.t_samples[m] : t + dt;
+                ++nstep;
+                if (sample) {
+                    const double mu0 = block_total(0), mu1 = block_total(1), mu2 = block_total(2);
+                    if (lane == 0) {
+                        double* r = kp.rec + ((size_t)s * kp.M + m) * 6;
+                        r[0] = t; r[1] = c; r[2] = mu0; r[3] = mu1; r[4] = mu2; r[5] = mu3;
+                        const double Lb = mu1 / mu0;
+                        const double rc = (c - tgt[2 * m]) / rms_c, rL = (Lb - tgt[2 * m + 1]) / rms_L;
+                        loss += rc * rc + rL * rL;
+                        const double gL = 2.0 * rL / rms_L;                 // d loss / d Lbar
+                        double* tr = trs + (size_t)k * ADJ_TR;
+                        tr[TR_LC] = 2.0 * rc / rms_c;
+                        tr[TR_L0] = -gL * mu1 / (mu0 * mu0);
+                        tr[TR_L1] = gL / mu0;
+                    }
+                }
+                if (landing) ++m;
+                if (m >= kp.M) go = false;
+                else if (nstep >= kp.max_steps) { status = ST_MAXSTEPS; go = false; }
+                else go = kinetics(k + 1);
+            }
+            if (lane == 0) { s_go = go; s_sample = go && landing; s_nsteps = nstep; }
+        }
+        __syncthreads();
+        q ^= 1;
+        ++k;
+    }
+    if (warp == 0 && lane == 0) {
+        kp.status[s] = status;
+        kp.steps[s] = nstep;
+        kp.loss[s] = status == ST_OK ? loss : __longlong_as_double(0x7ff8000000000000ll);
+        s_ok = status == ST_OK;
+    }
+    __syncthreads();
+    const double* th = kp.theta + (size_t)s * kp.n_params;
+    if (!s_ok) {
+        for (int j = tid; j < kp.n_params; j += NT) ap.gtheta[(size_t)s * kp.n_params + j] = __longlong_as_double(0x7ff8000000000000ll);
+        return;
+    }
+    const long long Ktot = s_nsteps;
+
+    // ---- reverse pass ---------------------------------------------------------------------------
+    double gacc[ADJ_GMAX];
+#pragma unroll
+    for (int g = 0; g < ADJ_GMAX; ++g) gacc[g] = 0.0;
+    auto theta_accumulate = [&](double lamG, double S, double T) {
+        if (kp.law == LAW_POLY) {                  // dG/da_j = (S-1)^(j+1): x^(tid+1) x (x^NT)^g
+            if (!(S > 1.0)) return;
+            const double X = S - 1.0;
+            double xp = pow(X, (double)(tid + 1));
+            const double xs = pow(X, (double)NT);
+#pragma unroll
+            for (int g = 0; g < ADJ_GMAX; ++g) {
+                if (tid + g * NT < kp.n_params) gacc[g] = fma(lamG, xp, gacc[g]);
+                xp *= xs;
+            }
+            return;
+        }
+        for (int j = tid; j < kp.n_params && j < 6; j += NT) gacc[0] = fma(lamG, dG_dtheta(kp, th, S, T, j), gacc[0]);
+    };
+    // warp-0 adjoint scalars: of c^{k+1} (before the sample term of step k), t^{k+1}, mu3p^{k+1}
+    double lam_c = 0.0, lam_t = 0.0, lam_mu = 0.0;
+    auto pre_step = [&](long long kk) {            // warp 0: broadcast what the vector phase of kk needs
+        const double* r = trs + (size_t)kk * ADJ_TR;
+        const double lcp = lam_c + r[TR_LC];
+        if (lane == 0) {
+            s_sc[SC_LM] = -rho * lcp + lam_mu;     // adjoint of mu3(n^{kk+1})
+            s_sc[SC_L0] = r[TR_L0]; s_sc[SC_L1] = r[TR_L1];
+            s_sc[SC_C] = r[TR_C]; s_sc[SC_KAP2] = r[TR_KAP2]; s_sc[SC_BETA2] = r[TR_BETA2];
+        }
+    };
+    int ql = 0;                                    // lb[ql] = lambda of n^{k+1} (raw)
+    bool have_lg = false;
+    double lg_prev = 0.0, S_prev = 0.0, T_prev = 0.0;
+    const long long nseg = (Ktot + Kseg - 1) / Kseg;
+    for (long long sg = nseg - 1; sg >= 0; --sg) {
+        const long long k0 = sg * Kseg, k1 = min(k0 + (long long)Kseg, Ktot);
+        // re-march the segment from its checkpoint (C^k from the trace): states n^{k0..k1}
+        {
+            const double* ckp = cks + (size_t)sg * N;
+#pragma unroll
+            for (int j = 0; j < K; ++j) if (i0 + j < N) nb[i0 + j + 2] = ckp[i0 + j];
+            __syncthreads();
+            int qq = 0;
+            for (long long kk = k0; kk < k1; ++kk) {
+                double* sp = sgs + (size_t)(kk - k0) * N;
+#pragma unroll
+                for (int j = 0; j < K; ++j) if (i0 + j < N) sp[i0 + j] = nb[qq * NP + i0 + j + 2];
+                const double* r = trs + (size_t)kk * ADJ_TR;
+                update(qq, r[TR_C], r[TR_KAP2], clip);
+                __syncthreads();
+                qq ^= 1;
+            }
+            double* sp = sgs + (size_t)(k1 - k0) * N;
+#pragma unroll
+            for (int j = 0; j < K; ++j) if (i0 + j < N) sp[i0 + j] = nb[qq * NP + i0 + j + 2];
+        }
+        if (warp == 0) pre_step(k1 - 1);
+        __syncthreads();
+        for (long long kk = k1 - 1; kk >= k0; --kk) {
+            // ---- vector phase: lambda^{kk+1} (+ mass-balance and sample terms, clip marks) ->
+            //      lambda^kk, partial lambda_C -------------------------------------------------
+            if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
+            const double C = s_sc[SC_C], kap2 = s_sc[SC_KAP2], beta2 = s_sc[SC_BETA2];
+            const double lm = s_sc[SC_LM], l0 = s_sc[SC_L0], l1 = s_sc[SC_L1];
+            const double* nk = sgs + (size_t)(kk - k0) * N;            // n^kk
+            const double* nk1 = nk + N;                                 // n^{kk+1}
+            const double* lin = lb + ql * NP + i0;                      // lin[j] = raw lambda of bin i0-2+j
+            double w[K + 4], lam[K + 4];
+#pragma unroll
+            for (int j = 0; j < K + 4; ++j) {
+                const int i = i0 - 2 + j;
+                const bool in = i >= 0 && i < N;
+                w[j] = in ? nk[i] : 0.0;
+                const double v1 = in ? nk1[i] : 0.0;
+                const bool clipped = in && v1 == 0.0 && signbit(v1);
+                double l = lin[j];
+                if (in) {
+                    const double L = fma((double)i, kp.dL, kp.L_lo + 0.5 * kp.dL);
+                    const double w0 = kp.dL, w1 = w0 * L, w3 = w1 * L * L;
+                    l = fma(lm, w3, fma(l1, w1, fma(l0, w0, l)));
+                }
+                lam[j] = (in && !clipped) ? l : 0.0;
+            }
+            // face partials (as k_resident's tangent lanes): faces f = i0 - 1 + e, e = 0..K+2
+            double Lf[K + 3], whi[K + 3], wmid[K + 3], wlo[K + 3];
+            double lamC = 0.0;
+#pragma unroll
+            for (int e = 0; e < K + 3; ++e) {
+                const int f = i0 - 1 + e;                                // face between bins f-1 | f
+                // window index of bin f: f - (i0 - 2) = e + 1
+                double a, b, nup;
+                if (C >= 0.0) {
+                    if (e < 1) { Lf[e] = 0.0; whi[e] = wmid[e] = wlo[e] = 0.0; continue; }
+                    a = w[e] - w[e - 1]; b = w[e + 1] - w[e]; nup = w[e];
+                } else {
+                    if (e > K + 1) { Lf[e] = 0.0; whi[e] = wmid[e] = wlo[e] = 0.0; continue; }
+                    a = w[e + 2] - w[e + 1]; b = w[e + 1] - w[e]; nup = w[e + 1];
+                }
+                double h = 0.0, qa = 0.0, qb = 0.0;
+                if (vl) psi_half_d(a, b, h, qa, qb);
+                const double pak = kap2 * qa, pbk = kap2 * qb;
+                if (C >= 0.0) { whi[e] = pbk; wmid[e] = C + (pak - pbk); wlo[e] = -pak; }
+                else          { whi[e] = pak; wmid[e] = C - (pak - pbk); wlo[e] = -pbk; }
+                Lf[e] = lam[e + 1] - lam[e];                             // lambda_f - lambda_{f-1}
+                const bool owned = (f >= i0 && f < i0 + K && f <= N) || (f == N && i0 + K == N);
+                if (owned) lamC = fma(Lf[e], fma(beta2, h, nup), lamC); // dF/dC = n_up + beta psi
+            }
+            double* lout = lb + (ql ^ 1) * NP + i0 + 2;
+#pragma unroll
+            for (int kq = 0; kq < K; ++kq) {
+                if (i0 + kq >= N) continue;
+                const int e = kq + 1;                                    // face index of face j = bin j
+                double v = lam[kq + 2];
+                if (C >= 0.0) v += Lf[e] * whi[e] + Lf[e + 1] * wmid[e + 1] + Lf[e + 2] * wlo[e + 2];
+                else          v += Lf[e + 1] * wlo[e + 1] + Lf[e] * wmid[e] + Lf[e - 1] * whi[e - 1];
+                lout[kq] = v;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) lamC += __shfl_xor_sync(0xffffffffu, lamC, off);
+            if (lane == 0) s_red[warp][0] = lamC;
+            __syncthreads();
+            // ---- scalar phase (warp 0): adjoints of c^kk, t^kk, mu3p^kk; lambda_G^kk ------------
+            if (warp == 0) {
+                const double* r = trs + (size_t)kk * ADJ_TR;
+                const double LC = block_total(0);
+                const double lcp = lam_c + r[TR_LC];
+                const double nc = lcp + LC * r[TR_CC] + lam_t * r[TR_TC];
+                const double nt = LC * r[TR_CT] + lam_t * r[TR_TT];
+                const double lG = LC * r[TR_CG] + lam_t * r[TR_TG];
+                lam_mu = rho * lcp;
+                lam_c = nc; lam_t = nt;
+                if (lane == 0) { s_sc[SC_LG] = lG; s_sc[SC_S] = r[TR_S]; s_sc[SC_T] = r[TR_T]; }
+                if (kk > k0) pre_step(kk - 1);
+            }
+            __syncthreads();
+            lg_prev = s_sc[SC_LG]; S_prev = s_sc[SC_S]; T_prev = s_sc[SC_T];
+            have_lg = true;
+            ql ^= 1;
+        }
+        __syncthreads();
+    }
+    if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
+#pragma unroll
+    for (int g = 0; g < ADJ_GMAX; ++g) {
+        const int j = tid + g * NT;
+        if (j < kp.n_params) ap.gtheta[(size_t)s * kp.n_params + j] = gacc[g];
+    }
+}
+
+}  // namespace pbe

@@ -20,6 +20,7 @@
 #include "k_stream.cuh"
 #include "k_2d.cuh"
 #include "k_2d_fused.cuh"
+#include "k_adjoint.cuh"
 #include "k_stream_tb.cuh"
 
 using pbe::KParams;
@@ -61,6 +62,9 @@ struct pbe_ctx_s {
     DevBuf rec, trec, status, steps, loss, grad;
     // streaming-kernel scratch (allocated on first use)
     DevBuf sbuf, spart, sbar, sfinal, snscale;
+    // adjoint (NEXT-3) scratch: step trace, checkpoints, segment states, dL/dtheta
+    DevBuf atr, ack, aseg, agrad;
+    bool last_adjoint = false;
     // last run
     bool have_run = false;
     int last_sims = 0;
@@ -454,6 +458,106 @@ static pbe_status launch_2d_fused(pbe_ctx ctx, KParams kp, int S, const double* 
 }
 
 // ------------------------------------------------------------------------------------
+// Run set-up shared by pbe_run_batch and pbe_run_adjoint
+// ------------------------------------------------------------------------------------
+// Argument checks (synchronous PBE_ERR_ARG).
+static pbe_status validate_run(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride,
+                               int32_t n0_on_device, const double* c0, const double* t_samples,
+                               const double* ndot_final) {
+    if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
+    if (!ctx->have_kin) return fail(ctx, PBE_ERR_STATE, "pbe_set_kinetics must precede pbe_run_batch");
+    const pbe_config& cf = ctx->cfg;
+    const int N = cf.n_bins, M = cf.n_samples, P = cf.n_tangents;
+    const bool steps_mode = cf.n_steps > 0;
+    if (n_sims < 1 || n_sims > cf.max_sims) return fail(ctx, PBE_ERR_ARG, "n_sims must be in [1, max_sims]");
+    if (n_sims != ctx->kin_sims) return fail(ctx, PBE_ERR_ARG, "n_sims (%d) != kinetics n_sims (%d)", n_sims, ctx->kin_sims);
+    if (!n0 || !c0) return fail(ctx, PBE_ERR_ARG, "NULL n0 or c0");
+    const bool two_d = cf.n_bins2 > 0;
+    const long long cells = (long long)N * (two_d ? cf.n_bins2 : 1);
+    if (n0_stride != 0 && n0_stride != cells) return fail(ctx, PBE_ERR_ARG, "n0_stride must be 0 or the cells per simulation");
+    if (!steps_mode && !t_samples) return fail(ctx, PBE_ERR_ARG, "NULL t_samples");
+    for (int s = 0; s < n_sims; ++s)
+        if (!(c0[s] >= 0.0) || !std::isfinite(c0[s])) return fail(ctx, PBE_ERR_ARG, "c0[%d] must be finite and >= 0", s);
+    if (!steps_mode) {
+        if (!(t_samples[0] > 0.0)) return fail(ctx, PBE_ERR_ARG, "t_samples[0] must be > 0");
+        for (int m = 1; m < M; ++m)
+            if (!(t_samples[m] > t_samples[m - 1])) return fail(ctx, PBE_ERR_ARG, "t_samples must be strictly increasing");
+        if (!std::isfinite(t_samples[M - 1])) return fail(ctx, PBE_ERR_ARG, "t_samples must be finite");
+    }
+    if (!n0_on_device) {
+        const size_t rows = n0_stride ? (size_t)n_sims : 1;
+        for (size_t j = 0; j < rows * (size_t)cells; ++j)
+            if (!(n0[j] >= 0.0) || !std::isfinite(n0[j])) return fail(ctx, PBE_ERR_ARG, "n0[%zu] must be finite and >= 0", j);
+    }
+    if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
+    (void)M;
+    return PBE_OK;
+}
+
+// Copies the run inputs on stream st (c0, sample times, target, host n0) and presets the
+// records to NaN (unreached samples).  *n0_dev: device n0 (caller's or staged).
+static pbe_status stage_run(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride,
+                            int32_t n0_on_device, const double* c0, const double* t_samples,
+                            const double* target, cudaStream_t st, const double** n0_dev_out) {
+    const pbe_config& cf = ctx->cfg;
+    const int N = cf.n_bins, M = cf.n_samples, P = cf.n_tangents;
+    const bool steps_mode = cf.n_steps > 0;
+    const bool two_d = cf.n_bins2 > 0;
+    const long long cells = (long long)N * (two_d ? cf.n_bins2 : 1);
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->c0.p, c0, n_sims * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (!steps_mode)
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->tsamp.p, t_samples, M * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (target) {
+        CUDA_TRY(ctx, ctx->target.ensure((size_t)n_sims * M * 2 * sizeof(double)));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->target.p, target, (size_t)n_sims * M * 2 * sizeof(double),
+                                      cudaMemcpyHostToDevice, st));
+    }
+    const double* n0_dev = n0;
+    if (!n0_on_device) {
+        const size_t bytes = (n0_stride ? (size_t)n_sims : 1) * (size_t)cells * sizeof(double);
+        CUDA_TRY(ctx, ctx->n0_staged.ensure(bytes));
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->n0_staged.p, n0, bytes, cudaMemcpyHostToDevice, st));
+        n0_dev = ctx->n0_staged.as<double>();
+    }
+    // unreached samples read as NaN (all-ones bytes)
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->rec.p, 0xff, (size_t)n_sims * M * (two_d ? 8 : 6) * sizeof(double), st));
+    if (P) CUDA_TRY(ctx, cudaMemsetAsync(ctx->trec.p, 0xff, (size_t)n_sims * M * P * 5 * sizeof(double), st));
+    *n0_dev_out = n0_dev;
+    return PBE_OK;
+}
+
+static KParams make_kparams(pbe_ctx ctx, int n_sims, const double* n0_dev, long long n0_stride,
+                            const double* target, double* n_final, double* ndot_final, int groups) {
+    const pbe_config& cf = ctx->cfg;
+    const int N = cf.n_bins, M = cf.n_samples, P = cf.n_tangents;
+    KParams kp{};
+    kp.N = N; kp.L_lo = cf.L_lo; kp.dL = cf.dL; kp.inv_dL = 1.0 / cf.dL; kp.limiter = cf.limiter;
+    kp.courant = cf.courant; kp.dt_fixed = cf.dt_fixed; kp.dt_max = cf.dt_max;
+    kp.max_steps = cf.max_steps; kp.n_steps = cf.n_steps; kp.rho_kv = cf.rho_c * cf.k_v;
+    kp.law = ctx->law; kp.n_params = ctx->n_params; kp.sol_kind = ctx->sol_kind; kp.n_sol = ctx->n_sol;
+    kp.n_knots = ctx->n_knots; kp.knotT_stride = ctx->knotT_per_sim ? ctx->n_knots : 0;
+    kp.theta = ctx->theta.as<double>(); kp.sol = ctx->sol.as<double>(); kp.knot_t = ctx->knot_t.as<double>();
+    kp.knot_T = ctx->knot_T.as<double>(); kp.seed = ctx->seed.as<double>();
+    kp.n_sims = n_sims; kp.M = M; kp.P = P; kp.G = groups;
+    kp.n0 = n0_dev; kp.n0_stride = n0_stride; kp.c0 = ctx->c0.as<double>();
+    kp.t_samples = ctx->tsamp.as<double>(); kp.target = target ? ctx->target.as<double>() : nullptr;
+    kp.rec = ctx->rec.as<double>(); kp.trec = ctx->trec.as<double>(); kp.status = ctx->status.as<int>();
+    kp.steps = ctx->steps.as<long long>(); kp.loss = ctx->loss.as<double>(); kp.grad = ctx->grad.as<double>();
+    kp.n_final = n_final; kp.ndot_final = ndot_final;
+    return kp;
+}
+
+// ------------------------------------------------------------------------------------
+// k_adjoint launch (NEXT-3): one CTA per simulation; K from N (smem: 4 (NT K + 4) doubles)
+// ------------------------------------------------------------------------------------
+struct AdjointVariant { int K; const void* fn; };
+const AdjointVariant kAdjoint[] = {
+    {4, (const void*)&pbe::k_adjoint<4>}, {8, (const void*)&pbe::k_adjoint<8>},
+    {16, (const void*)&pbe::k_adjoint<16>}, {24, (const void*)&pbe::k_adjoint<24>},
+};
+
+// ------------------------------------------------------------------------------------
 // C ABI
 // ------------------------------------------------------------------------------------
 extern "C" {
@@ -534,7 +638,7 @@ void pbe_destroy(pbe_ctx ctx) {
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->theta, &ctx->sol, &ctx->knot_t, &ctx->knot_T, &ctx->seed, &ctx->c0, &ctx->tsamp,
                       &ctx->target, &ctx->n0_staged, &ctx->rec, &ctx->trec, &ctx->status, &ctx->steps,
-                      &ctx->loss, &ctx->grad, &ctx->sbuf, &ctx->spart, &ctx->sbar, &ctx->sfinal, &ctx->snscale})
+                      &ctx->loss, &ctx->grad, &ctx->sbuf, &ctx->spart, &ctx->sbar, &ctx->sfinal, &ctx->snscale, &ctx->atr, &ctx->ack, &ctx->aseg, &ctx->agrad})
         b->release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -547,7 +651,7 @@ pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t 
                             const double* tangent_seed) {
     if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
     if (law < PBE_LAW_CONST || law > PBE_LAW_POLY) return fail(ctx, PBE_ERR_ARG, "unknown law %d", law);
-    if (n_params < 1 || n_params > pbe::MAXTH) return fail(ctx, PBE_ERR_ARG, "n_params must be in [1, 10]");
+    if (n_params < 1 || n_params > pbe::MAX_PARAMS) return fail(ctx, PBE_ERR_ARG, "n_params must be in [1, %d]", pbe::MAX_PARAMS);
     const bool two_d = ctx->cfg.n_bins2 > 0;
     if (two_d && (n_params % 2) != 0) return fail(ctx, PBE_ERR_ARG, "2D mode: theta = [dim-1 law | dim-2 law] (even n_params)");
     const int per_dim = two_d ? n_params / 2 : n_params;
@@ -592,32 +696,14 @@ pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t 
 pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride, int32_t n0_on_device,
                          const double* c0, const double* t_samples, const double* target, double* n_final,
                          double* ndot_final, void* cuda_stream) {
-    if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
-    if (!ctx->have_kin) return fail(ctx, PBE_ERR_STATE, "pbe_set_kinetics must precede pbe_run_batch");
+    {
+        const pbe_status v = validate_run(ctx, n_sims, n0, n0_stride, n0_on_device, c0, t_samples, ndot_final);
+        if (v != PBE_OK) return v;
+    }
     const pbe_config& cf = ctx->cfg;
-    const int N = cf.n_bins, M = cf.n_samples, P = cf.n_tangents;
-    const bool steps_mode = cf.n_steps > 0;
-    if (n_sims < 1 || n_sims > cf.max_sims) return fail(ctx, PBE_ERR_ARG, "n_sims must be in [1, max_sims]");
-    if (n_sims != ctx->kin_sims) return fail(ctx, PBE_ERR_ARG, "n_sims (%d) != kinetics n_sims (%d)", n_sims, ctx->kin_sims);
-    if (!n0 || !c0) return fail(ctx, PBE_ERR_ARG, "NULL n0 or c0");
+    const int N = cf.n_bins, P = cf.n_tangents;
     const bool two_d = cf.n_bins2 > 0;
-    const long long cells = (long long)N * (two_d ? cf.n_bins2 : 1);
-    if (n0_stride != 0 && n0_stride != cells) return fail(ctx, PBE_ERR_ARG, "n0_stride must be 0 or the cells per simulation");
-    if (!steps_mode && !t_samples) return fail(ctx, PBE_ERR_ARG, "NULL t_samples");
-    for (int s = 0; s < n_sims; ++s)
-        if (!(c0[s] >= 0.0) || !std::isfinite(c0[s])) return fail(ctx, PBE_ERR_ARG, "c0[%d] must be finite and >= 0", s);
-    if (!steps_mode) {
-        if (!(t_samples[0] > 0.0)) return fail(ctx, PBE_ERR_ARG, "t_samples[0] must be > 0");
-        for (int m = 1; m < M; ++m)
-            if (!(t_samples[m] > t_samples[m - 1])) return fail(ctx, PBE_ERR_ARG, "t_samples must be strictly increasing");
-        if (!std::isfinite(t_samples[M - 1])) return fail(ctx, PBE_ERR_ARG, "t_samples must be finite");
-    }
-    if (!n0_on_device) {
-        const size_t rows = n0_stride ? (size_t)n_sims : 1;
-        for (size_t j = 0; j < rows * (size_t)cells; ++j)
-            if (!(n0[j] >= 0.0) || !std::isfinite(n0[j])) return fail(ctx, PBE_ERR_ARG, "n0[%zu] must be finite and >= 0", j);
-    }
-    if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
+    const bool steps_mode = cf.n_steps > 0;
 
     // kernel choice: register-resident when the simulation fits one CTA, else streaming
     int groups = 1;
@@ -645,40 +731,12 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
         return fail(ctx, PBE_ERR_ARG, "the streaming kernel supports at most 4 tangent lanes (got %d)", P);
 
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->c0.p, c0, n_sims * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (!steps_mode)
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->tsamp.p, t_samples, M * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (target) {
-        CUDA_TRY(ctx, ctx->target.ensure((size_t)n_sims * M * 2 * sizeof(double)));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->target.p, target, (size_t)n_sims * M * 2 * sizeof(double),
-                                      cudaMemcpyHostToDevice, st));
+    const double* n0_dev = nullptr;
+    {
+        const pbe_status v = stage_run(ctx, n_sims, n0, n0_stride, n0_on_device, c0, t_samples, target, st, &n0_dev);
+        if (v != PBE_OK) return v;
     }
-    const double* n0_dev = n0;
-    if (!n0_on_device) {
-        const size_t bytes = (n0_stride ? (size_t)n_sims : 1) * (size_t)cells * sizeof(double);
-        CUDA_TRY(ctx, ctx->n0_staged.ensure(bytes));
-        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->n0_staged.p, n0, bytes, cudaMemcpyHostToDevice, st));
-        n0_dev = ctx->n0_staged.as<double>();
-    }
-    // unreached samples read as NaN (all-ones bytes)
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->rec.p, 0xff, (size_t)n_sims * M * (two_d ? 8 : 6) * sizeof(double), st));
-    if (P) CUDA_TRY(ctx, cudaMemsetAsync(ctx->trec.p, 0xff, (size_t)n_sims * M * P * 5 * sizeof(double), st));
-
-    KParams kp{};
-    kp.N = N; kp.L_lo = cf.L_lo; kp.dL = cf.dL; kp.inv_dL = 1.0 / cf.dL; kp.limiter = cf.limiter;
-    kp.courant = cf.courant; kp.dt_fixed = cf.dt_fixed; kp.dt_max = cf.dt_max;
-    kp.max_steps = cf.max_steps; kp.n_steps = cf.n_steps; kp.rho_kv = cf.rho_c * cf.k_v;
-    kp.law = ctx->law; kp.n_params = ctx->n_params; kp.sol_kind = ctx->sol_kind; kp.n_sol = ctx->n_sol;
-    kp.n_knots = ctx->n_knots; kp.knotT_stride = ctx->knotT_per_sim ? ctx->n_knots : 0;
-    kp.theta = ctx->theta.as<double>(); kp.sol = ctx->sol.as<double>(); kp.knot_t = ctx->knot_t.as<double>();
-    kp.knot_T = ctx->knot_T.as<double>(); kp.seed = ctx->seed.as<double>();
-    kp.n_sims = n_sims; kp.M = M; kp.P = P; kp.G = groups;
-    kp.n0 = n0_dev; kp.n0_stride = n0_stride; kp.c0 = ctx->c0.as<double>();
-    kp.t_samples = ctx->tsamp.as<double>(); kp.target = target ? ctx->target.as<double>() : nullptr;
-    kp.rec = ctx->rec.as<double>(); kp.trec = ctx->trec.as<double>(); kp.status = ctx->status.as<int>();
-    kp.steps = ctx->steps.as<long long>(); kp.loss = ctx->loss.as<double>(); kp.grad = ctx->grad.as<double>();
-    kp.n_final = n_final; kp.ndot_final = ndot_final;
+    KParams kp = make_kparams(ctx, n_sims, n0_dev, n0_stride, target, n_final, ndot_final, groups);
 
     ctx->info = pbe_run_info{};
     ctx->info.steps_per_pass = 1;
@@ -738,6 +796,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     ctx->have_run = true;
     ctx->last_sims = n_sims;
     ctx->last_stream = st;
+    ctx->last_adjoint = false;
     return PBE_OK;
 }
 
@@ -779,8 +838,93 @@ pbe_status pbe_tangents(pbe_ctx ctx, double* tangents, double* grad, int32_t on_
     if (r != PBE_OK) return r;
     const size_t S = ctx->last_sims, M = ctx->cfg.n_samples, P = ctx->cfg.n_tangents;
     if (P == 0) return fail(ctx, PBE_ERR_STATE, "context has no tangent lanes");
+    if (ctx->last_adjoint) return fail(ctx, PBE_ERR_STATE, "the last run was pbe_run_adjoint (no tangent records)");
     if ((r = copy_out(ctx, tangents, ctx->trec.p, S * M * P * 5 * sizeof(double), on_device)) != PBE_OK) return r;
     if ((r = copy_out(ctx, grad, ctx->grad.p, S * P * sizeof(double), on_device)) != PBE_OK) return r;
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->last_stream));
+    return PBE_OK;
+}
+
+pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride, int32_t n0_on_device,
+                           const double* c0, const double* t_samples, const double* target, int32_t checkpoint_every,
+                           void* cuda_stream) {
+    {
+        const pbe_status v = validate_run(ctx, n_sims, n0, n0_stride, n0_on_device, c0, t_samples, nullptr);
+        if (v != PBE_OK) return v;
+    }
+    const pbe_config& cf = ctx->cfg;
+    const int N = cf.n_bins;
+    if (cf.n_bins2 > 0) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: 1D model only");
+    if (cf.n_steps > 0) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: needs sample mode (n_steps = 0)");
+    if (!target) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: needs a target (the loss to differentiate)");
+    if (checkpoint_every < 0) return fail(ctx, PBE_ERR_ARG, "checkpoint_every must be >= 0");
+    const AdjointVariant* av = nullptr;
+    int nt = 0;
+    size_t smem = 0;
+    for (const auto& v : kAdjoint) {
+        const int t = ((N + v.K - 1) / v.K + 31) / 32 * 32;
+        const size_t sm = (size_t)4 * (t * v.K + 4) * sizeof(double);
+        if (t <= 256 && sm <= 200 * 1024) { av = &v; nt = t; smem = sm; break; }
+    }
+    if (!av) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: N = %d exceeds the adjoint kernel (N <= 6144)", N);
+    if (ctx->n_params > nt * pbe::ADJ_GMAX)
+        return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: %d parameters exceed %d for N = %d", ctx->n_params, nt * pbe::ADJ_GMAX, N);
+    const long long ms = cf.max_steps;
+    int Kseg = checkpoint_every;
+    if (Kseg == 0) Kseg = std::max(8, (int)std::ceil(std::sqrt((double)ms)));       // O(sqrt) memory
+    const long long n_ck = (ms + Kseg - 1) / Kseg;
+    const size_t tr_b = (size_t)n_sims * ms * pbe::ADJ_TR * sizeof(double);
+    const size_t ck_b = (size_t)n_sims * n_ck * N * sizeof(double);
+    const size_t sg_b = (size_t)n_sims * (Kseg + 1) * N * sizeof(double);
+    if ((double)tr_b + ck_b + sg_b > 64.0 * (1ull << 30))
+        return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: trace + checkpoints need %.1f GB (> 64 GB): lower max_steps or n_sims",
+                    ((double)tr_b + ck_b + sg_b) / (1ull << 30));
+
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const double* n0_dev = nullptr;
+    {
+        const pbe_status v = stage_run(ctx, n_sims, n0, n0_stride, n0_on_device, c0, t_samples, target, st, &n0_dev);
+        if (v != PBE_OK) return v;
+    }
+    CUDA_TRY(ctx, ctx->atr.ensure(tr_b));
+    CUDA_TRY(ctx, ctx->ack.ensure(ck_b));
+    CUDA_TRY(ctx, ctx->aseg.ensure(sg_b));
+    CUDA_TRY(ctx, ctx->agrad.ensure((size_t)n_sims * ctx->n_params * sizeof(double)));
+    pbe::AdjParams ap{};
+    ap.kp = make_kparams(ctx, n_sims, n0_dev, n0_stride, target, nullptr, nullptr, 1);
+    ap.kp.P = 0;
+    ap.ck = ctx->ack.as<double>(); ap.seg = ctx->aseg.as<double>(); ap.tr = ctx->atr.as<double>();
+    ap.gtheta = ctx->agrad.as<double>(); ap.n_ck = n_ck; ap.Kseg = Kseg;
+    CUDA_TRY(ctx, cudaFuncSetAttribute(av->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ctx->info = pbe_run_info{};
+    void* args[] = {&ap};
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    CUDA_TRY(ctx, cudaLaunchKernel(av->fn, dim3(n_sims), dim3(nt), args, smem, st));
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+    ctx->info.kernel = PBE_KERNEL_ADJOINT;
+    ctx->info.launches = 1;
+    ctx->info.threads_per_cta = nt;
+    ctx->info.ctas = n_sims;
+    ctx->info.cluster = 1;
+    ctx->info.bins_per_thread = av->K;
+    ctx->info.steps_per_pass = 1;
+    ctx->info.main_ms = -1.0;
+    ctx->have_run = true;
+    ctx->last_sims = n_sims;
+    ctx->last_stream = st;
+    ctx->last_adjoint = true;
+    return PBE_OK;
+}
+
+pbe_status pbe_adjoint_gradient(pbe_ctx ctx, double* grad, double* loss, int32_t on_device) {
+    if (!ctx) return fail(nullptr, PBE_ERR_ARG, "NULL context");
+    if (!ctx->have_run || !ctx->last_adjoint) return fail(ctx, PBE_ERR_STATE, "pbe_run_adjoint must precede pbe_adjoint_gradient");
+    pbe_status r = finish_run(ctx);
+    if (r != PBE_OK) return r;
+    const size_t S = ctx->last_sims;
+    if ((r = copy_out(ctx, grad, ctx->agrad.p, S * ctx->n_params * sizeof(double), on_device)) != PBE_OK) return r;
+    if ((r = copy_out(ctx, loss, ctx->loss.p, S * sizeof(double), on_device)) != PBE_OK) return r;
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->last_stream));
     return PBE_OK;
 }

@@ -20,7 +20,8 @@
 namespace pbe {
 
 constexpr int MAXP = 10;   // tangent lanes
-constexpr int MAXTH = 10;  // kinetic parameters
+constexpr int MAXTH = 10;  // kinetic parameters held in registers (POLY may have more: runtime loop)
+constexpr int MAX_PARAMS = 4096;   // PBE_MAX_PARAMS (include/pbe.h)
 
 enum { LIM_UPWIND = 0, LIM_VANLEER = 1 };
 enum { LAW_CONST = 0, LAW_ARRH = 1, LAW_POLY = 2 };
@@ -148,9 +149,14 @@ __device__ __forceinline__ D1 growth_rate(const KParams& kp, const KinLoader& L,
         return mk(0.0);
     }
     if (S.v > 1.0) {                                                      // eq-poly_growth_rate
+        const D1 x = S - 1.0;
+        if (kp.n_params > MAXTH) {        // long polynomials (NEXT-3: up to PBE_MAX_PARAMS terms)
+            D1 g = mk(0.0);
+            for (int j = kp.n_params - 1; j >= 0; --j) g = g * x + L.theta(j);
+            return g * x;
+        }
         // sum_{j=1..k} a_j x^j in Horner form (short dependency chain on the step's critical
         // path); parameters are loaded up front (independent of the chain)
-        const D1 x = S - 1.0;
         D1 a[MAXTH];
 #pragma unroll
         for (int j = 0; j < MAXTH; ++j) a[j] = (j < kp.n_params) ? L.theta(j) : mk(0.0);

@@ -1,0 +1,160 @@
+"""NEXT-3 parity: the reverse-mode gradient of libpbe (pbe_run_adjoint, k_adjoint) against the
+oracle's forward-mode gradient of the same discrete loss (oracle/pbe_oracle.cpp in dual
+arithmetic, pinned against complex-step and finite differences in test_oracle_pins.py).
+Reverse and forward mode differentiate the same discrete march with the same branch decisions,
+so they agree up to rounding: the bar is 1e-8 x max |grad| per simulation (R-21 style, the
+kinetic partials span many orders of magnitude) plus the loss to 1e-10 relative.
+Dual lanes are limited to 10, so the oracle gradient over n_params > 10 parameters is
+assembled from ceil(n_params / 10) runs with unit seed blocks."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+RTOL_GRAD = 1e-8
+RTOL_LOSS = 1e-10
+
+
+def oracle_grad(w):
+    """(loss [S], grad [S][n_params]) of workload w from the oracle in dual arithmetic."""
+    P, Q = w.n_params, w.sol.shape[0]
+    grads = []
+    loss = None
+    for j0 in range(0, P, 10):
+        nl = min(10, P - j0)
+        seed = np.zeros((nl, P + Q))
+        seed[np.arange(nl), j0 + np.arange(nl)] = 1.0
+        wk = W.replace(w, n_tangents=nl, tangent_seed=seed)
+        o = oracle.run(wk, oracle.MODE_DUAL, threads=8, want_n=False)
+        assert (o["status"] == 0).all(), o["status"]
+        lo, g = oracle.loss_and_grad(o["samples"], o["tsamples"], w.target)
+        loss = lo if loss is None else loss
+        grads.append(g)
+    return loss, np.concatenate(grads, axis=1)
+
+
+def gpu_adjoint(w, checkpoint_every=0):
+    import torch
+
+    import paper_2411_00742_b200 as pb
+    wg = W.replace(w, n_tangents=0, tangent_seed=None)
+    ctx = pb.context_for(wg)
+    n0 = torch.from_numpy(np.ascontiguousarray(w.n0)).cuda()
+    ctx.run_adjoint(n0, w.c0, w.t_samples, w.target, checkpoint_every=checkpoint_every)
+    g = ctx.adjoint_gradient(w.n_params)
+    rec = ctx.moments()
+    info = ctx.last_run_info()
+    ctx.close()
+    return g, rec, info
+
+
+def _check(w, checkpoint_every=0):
+    lo, go = oracle_grad(w)
+    g, rec, info = gpu_adjoint(w, checkpoint_every)
+    assert info["kernel"] == 5
+    assert (rec["status"] == 0).all(), rec["status"]
+    assert np.all(np.abs(g["loss"] - lo) <= RTOL_LOSS * np.abs(lo)), (g["loss"], lo)
+    scale = np.max(np.abs(go), axis=1, keepdims=True)
+    err = np.abs(g["grad"] - go) / scale
+    assert err.max() <= RTOL_GRAD, f"max grad err {err.max():.3e} (per-sim scale {scale.ravel()})"
+    return g, go
+
+
+def small_ensemble(n_params=8, n_sims=9, N=200, t_max=60.0, M=30, dt_max=0.5, limiter=W.LIM_VANLEER):
+    """C5-shaped (App. B experiments, polynomial growth) at test size; parameters beyond the
+    8 of POLY_A get small coefficients so the long polynomial stays physical."""
+    w = W.c5_ensemble(n_sims=n_sims, N=N, t_max=t_max, M=M, dt_max=dt_max, n_tangents=0)
+    if n_params != w.n_params:
+        th = np.zeros((n_sims, n_params))
+        k = min(n_params, w.n_params)
+        th[:, :k] = w.theta[:, :k]
+        if n_params > w.n_params:
+            rng = np.random.Generator(np.random.PCG64(7))
+            th[:, w.n_params:] = 0.05 * rng.random((n_sims, n_params - w.n_params))
+        w = W.replace(w, theta=th)
+    return W.replace(w, limiter=limiter, max_steps=20000)
+
+
+def test_adjoint_poly_ensemble_matches_oracle():
+    _check(small_ensemble())
+
+
+def test_adjoint_long_polynomial_matches_oracle():
+    """n_params = 40 > MAXTH: the runtime-loop POLY path on both sides."""
+    _check(small_ensemble(n_params=40, n_sims=3))
+
+
+def test_adjoint_upwind_matches_oracle():
+    _check(small_ensemble(n_sims=3, limiter=W.LIM_UPWIND))
+
+
+def test_adjoint_uncapped_cfl_matches_oracle():
+    """dt = nu dL/|G| (C = nu sgn G, R-9): the parameters act through the clock only."""
+    _check(small_ensemble(n_sims=3, dt_max=math.inf, t_max=120.0, M=12))
+
+
+def test_adjoint_dissolution_ramp_matches_oracle():
+    """C2-shaped: Arrhenius growth + dissolution (6 parameters), temperature ramp (dG/dt via
+    T(t)), C < 0 sweeps, landing steps."""
+    w = W.c2_dissolution()
+    N = 150
+    dL = 1200.0 / N
+    t = np.linspace(4.0, 120.0, 30)
+    w = W.replace(w, N=N, dL=dL, n0=W.gaussian_seed(N, dL, m0=3.0)[None, :], t_samples=t, dt_max=0.5,
+                  target=W._target(w.c0, t), max_steps=20000)
+    _check(w)
+
+
+def test_adjoint_fixed_dt_constant_growth_matches_oracle():
+    w = W.c1_growth(W.LIM_VANLEER, N=100, M=25)
+    t = np.linspace(8.0, 200.0, 25)
+    w = W.replace(w, t_samples=t, target=W._target(w.c0, t), max_steps=5000)
+    _check(w)
+
+
+def test_adjoint_checkpoint_interval_is_bitwise_neutral():
+    w = small_ensemble(n_sims=2, M=10, t_max=20.0)
+    g1, _, _ = gpu_adjoint(w, checkpoint_every=1)
+    g7, _, _ = gpu_adjoint(w, checkpoint_every=7)
+    g0, _, _ = gpu_adjoint(w, checkpoint_every=0)
+    assert np.array_equal(g1["grad"], g7["grad"]) and np.array_equal(g1["grad"], g0["grad"])
+
+
+def test_adjoint_agrees_with_gpu_tangents():
+    """The two GPU differentiation modes (k_resident tangent lanes, k_adjoint) agree."""
+    import paper_2411_00742_b200 as pb
+    w = small_ensemble(n_sims=4)
+    wt = W.replace(w, n_tangents=8)
+    r = pb.run_workload(wt, want_n=False)
+    g, rec, _ = gpu_adjoint(w)
+    scale = np.max(np.abs(r["grad"]), axis=1, keepdims=True)
+    assert (np.abs(g["grad"] - r["grad"]) / scale).max() <= RTOL_GRAD
+    ok = ~np.isnan(r["samples"])
+    assert np.allclose(rec["moments"][ok], r["samples"][ok], rtol=1e-12, atol=0)
+
+
+def test_adjoint_failed_simulation_gives_nan():
+    """A simulation that exceeds max_steps has no gradient (NaN) and status MAXSTEPS."""
+    w = W.replace(small_ensemble(n_sims=2), max_steps=50)
+    g, rec, _ = gpu_adjoint(w)
+    assert (rec["status"] == 5).all()
+    assert np.isnan(g["grad"]).all() and np.isnan(g["loss"]).all()
+
+
+def test_adjoint_rejects_bad_arguments():
+    import torch
+
+    import paper_2411_00742_b200 as pb
+    w = small_ensemble(n_sims=1)
+    ctx = pb.context_for(w)
+    n0 = torch.from_numpy(np.ascontiguousarray(w.n0)).cuda()
+    with pytest.raises(pb.PBEError):
+        ctx.run_adjoint(n0, w.c0, w.t_samples, None)                       # no target
+    with pytest.raises(pb.PBEError):
+        ctx.adjoint_gradient(w.n_params)                                   # no adjoint run yet
+    ctx.close()

@@ -414,6 +414,42 @@ def main():
         ctx4.close()
         del n04
 
+    # ---- NEXT-3 (1 GPU): one reverse-mode gradient over 1000 parameters (9 App-B experiments) vs the
+    #      batched forward-difference gradient (the paper's jax-ND analogue) --------
+    next3 = None
+    if world == 1 and args.workload == "c5" and not args.no_secondary:
+        P3 = 1000
+        w3 = W.next3_estimation(n_params=P3)
+        n03 = torch.from_numpy(np.ascontiguousarray(w3.n0)).to(dev)
+        ctx3 = pb.context_for(w3, device=local_rank)
+        ta = []
+        for it in range(3):
+            torch.cuda.synchronize(); t0 = time.perf_counter()
+            ctx3.run_adjoint(n03, w3.c0, w3.t_samples, w3.target)
+            g3 = ctx3.adjoint_gradient(P3)
+            torch.cuda.synchronize(); ta.append(time.perf_counter() - t0)
+        r3 = ctx3.moments()
+        ctx3.close()
+        h = 1e-6
+        th = np.repeat(w3.theta, P3 + 1, axis=0)
+        for si in range(w3.n_sims):
+            blk = th[si * (P3 + 1):(si + 1) * (P3 + 1)]
+            blk[1 + np.arange(P3), np.arange(P3)] += h * np.maximum(np.abs(w3.theta[si]), 1e-3)
+        wf = W.replace(w3, theta=th, c0=np.repeat(w3.c0, P3 + 1), knot_T=np.repeat(w3.knot_T, P3 + 1, axis=0),
+                       target=np.repeat(w3.target, P3 + 1, axis=0))
+        ctxf = pb.context_for(wf, device=local_rank)
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        ctxf.run_batch(n03, wf.c0, wf.t_samples, wf.target)
+        ctxf.moments()
+        torch.cuda.synchronize(); tf = time.perf_counter() - t0
+        ctxf.close()
+        next3 = dict(workload=f"NEXT-3: d loss/d theta, {P3} POLY parameters, 9 App-B experiments, N={w3.N}, "
+                              f"{int(r3['steps'].max())} steps", metric="ms per gradient (wall, incl. copies)",
+                     adjoint_ms=1e3 * min(ta), fd_batched_ms=1e3 * tf, fd_sims=int(wf.n_sims),
+                     speedup_vs_fd=tf / min(ta), finite=bool(np.isfinite(g3["grad"]).all()),
+                     note="forward-mode tangents need 100 passes of 10 lanes (tools/next3_time.py: 92x slower)")
+        del n03
+
     # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -430,7 +466,7 @@ def main():
                     ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
                     data="synthetic (seeded; DESIGN.md input recipe)", config=cfg, roofline=roof,
                     cpu_baseline=cpu, e2e=e2e, gpu_launches=int(info["launches"]) * args.steps, clocks=clk,
-                    secondary=secondary)
+                    secondary=secondary, next3=next3)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

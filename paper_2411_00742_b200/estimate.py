@@ -9,7 +9,9 @@ B200 design: R independent estimations (e.g. multi-start) advance together.  One
 iteration = ONE pbe_run_batch of R x 9 simulations with k forward-mode tangent lanes (one
 per coefficient) — the loss of every simulation and its exact gradient come out of the same
 launch (row a7/a8) — then the Adam update of the R parameter vectors (host, R x k numbers).
-No finite differences and no reverse pass are needed for k <= 10.
+No finite differences and no reverse pass are needed for k <= 10.  For more coefficients
+(the paper's 1000-parameter regime, L599) grad_mode="adjoint" takes the gradient from the
+discrete adjoint instead (pbe_run_adjoint, NEXT-3): same loss, cost independent of k.
 
 In-silico data (R-28): the paper generated its targets with the method of moments and the
 Arrhenius truth (L741-743).  Here the targets are produced by the same FVM march with the
@@ -102,18 +104,24 @@ class Estimator:
     theta0: np.ndarray                      # [R][k] initial parameters (>= 0)
     lr: float = 0.01
     device: int = 0
+    grad_mode: str = "auto"                 # "tangent" (k <= 10), "adjoint", "auto"
     history: list = field(default_factory=list)
 
     def __post_init__(self):
         import torch
         self.theta0 = np.atleast_2d(np.asarray(self.theta0, dtype=np.float64))
         self.R, self.k = self.theta0.shape
-        if self.k > 10:
-            raise ValueError("at most 10 parameters (tangent lanes)")
+        if self.grad_mode == "auto":
+            self.grad_mode = "tangent" if self.k <= 10 else "adjoint"
+        if self.grad_mode == "tangent" and self.k > 10:
+            raise ValueError("at most 10 parameters with tangent lanes (use grad_mode='adjoint')")
         e = self.exps
         M = e.t_samples.shape[0]
-        self.ctx = Context(e.N, e.dL, dt_max=e.dt_max, n_samples=M, n_tangents=self.k,
-                           max_sims=self.R * 9, device=self.device, rho_c=e.rho_c, k_v=e.k_v)
+        adj = self.grad_mode == "adjoint"
+        # the adjoint's trace is sized by max_steps: bound it by the sample horizon
+        max_steps = int(1.2 * e.t_samples[-1] / e.dt_max) + 1000 if adj else 10_000_000
+        self.ctx = Context(e.N, e.dL, dt_max=e.dt_max, n_samples=M, n_tangents=0 if adj else self.k,
+                           max_sims=self.R * 9, device=self.device, rho_c=e.rho_c, k_v=e.k_v, max_steps=max_steps)
         self.n0 = torch.from_numpy(np.ascontiguousarray(e.n0[None, :])).cuda(self.device)
         self.c0 = np.tile(e.c0, self.R)
         self.T = np.tile(e.T, self.R)[:, None]
@@ -126,9 +134,14 @@ class Estimator:
         e = self.exps
         th = np.repeat(theta, 9, axis=0)                    # sim r*9 + j runs fit r on experiment j
         self.ctx.set_kinetics(LAW_POLY, th, SOL_EXP, np.array(e.sol), np.array([0.0]), self.T)
-        self.ctx.run_batch(self.n0, self.c0, e.t_samples, self.target)
-        out = self.ctx.moments()
-        g = self.ctx.tangents()["grad"]
+        if self.grad_mode == "adjoint":
+            self.ctx.run_adjoint(self.n0, self.c0, e.t_samples, self.target)
+            g = self.ctx.adjoint_gradient(self.k)["grad"]
+            out = self.ctx.moments()
+        else:
+            self.ctx.run_batch(self.n0, self.c0, e.t_samples, self.target)
+            out = self.ctx.moments()
+            g = self.ctx.tangents()["grad"]
         ok = out["status"] == 0
         loss = np.where(ok, out["loss"], np.inf).reshape(self.R, 9).sum(axis=1)
         grad = np.where(ok[:, None], g, 0.0).reshape(self.R, 9, self.k).sum(axis=1)

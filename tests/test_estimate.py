@@ -93,3 +93,35 @@ def test_multistart_estimation_reduces_loss(exps):
     assert np.all(np.isfinite(loss)) and np.all(theta >= 0)
     assert np.all(loss < 0.5 * l0), (l0, loss)
     est.close()
+
+
+@pytest.mark.gpu
+def test_adjoint_estimator_matches_tangent_estimator(exps):
+    """grad_mode='adjoint' (NEXT-3) drives the same Adam trajectory as the tangent lanes."""
+    from paper_2411_00742_b200.estimate import Estimator
+    et = Estimator(exps, THETA0, grad_mode="tangent")
+    ea = Estimator(exps, THETA0, grad_mode="adjoint")
+    lt, gt, _ = et.loss_and_grad(THETA0)
+    la, ga, _ = ea.loss_and_grad(THETA0)
+    assert np.allclose(la, lt, rtol=1e-12, atol=0)
+    assert np.allclose(ga, gt, rtol=1e-9, atol=1e-12 * np.abs(gt).max())
+    et.run(3); ea.run(3)
+    for it in range(4):
+        assert np.allclose(ea.history[it]["theta"], et.history[it]["theta"], rtol=1e-9, atol=0), it
+    et.close(); ea.close()
+
+
+@pytest.mark.gpu
+def test_adjoint_estimator_many_coefficients(exps):
+    """40 polynomial coefficients (beyond the 10 tangent lanes): Adam on adjoint gradients
+    lowers the RSS."""
+    from paper_2411_00742_b200.estimate import Estimator
+    th0 = np.zeros((2, 40))
+    th0[:, :4] = THETA0 * np.array([[1.0], [1.3]])
+    th0[:, 4:] = 0.01
+    est = Estimator(exps, th0, lr=0.05)
+    assert est.grad_mode == "adjoint"
+    theta, loss = est.run(20)
+    assert np.all(np.isfinite(loss)) and np.all(theta >= 0)
+    assert np.all(loss < est.history[0]["loss"]), (est.history[0]["loss"], loss)
+    est.close()

@@ -217,6 +217,30 @@ def c5_ensemble(n_sims: int = 4096, N: int = 2000, t_max: float = 600.0, M: int 
         target=_target(c0, t), n_tangents=n_tangents)
 
 
+def next3_estimation(n_params: int = 1000, N: int = 2000, t_max: float = 600.0, M: int = 600,
+                     dt_max: float = 0.05, seed: int = 599) -> Workload:
+    """NEXT-3: the paper's parameter-estimation regime with many parameters (L565-572: the
+    polynomial is lengthened to raise the parameter count; L599: 1000 parameters).  The 9 App-B
+    experiments (L734-744), one simulation each, POLY growth with a_1..a_8 = POLY_A and
+    a_9..a_n drawn U(0, 0.05) (PCG64 `seed`), C5's grid and clock, target as C5."""
+    dL = 1200.0 / N
+    rng = np.random.Generator(np.random.PCG64(seed))
+    theta = np.zeros((9, n_params))
+    k = min(n_params, len(POLY_A))
+    theta[:, :k] = np.array(POLY_A)[:k]
+    if n_params > k:
+        theta[:, k:] = 0.05 * rng.random((9, n_params - k))
+    e = np.arange(9)
+    T = np.array(APPB_T)[e // 3]
+    c0 = np.array(APPB_S0)[e % 3] * np.array(APPB_CSAT)[e // 3]
+    t = np.linspace(t_max / M, t_max, M)
+    return Workload(
+        name=f"next3_estimation_P{n_params}_N{N}", N=N, dL=dL, dt_max=dt_max, max_steps=int(1.2 * t_max / dt_max) + 1000,
+        law=LAW_POLY, theta=theta, sol_kind=SOL_EXP, sol=np.array(SOL_EXP_DEFAULT),
+        knot_t=np.array([0.0]), knot_T=T[:, None].copy(),
+        n0=gaussian_seed(N, dL, m0=1.0)[None, :], c0=c0, t_samples=t, target=_target(c0, t))
+
+
 CONFIGS = {
     "c1": c1_growth,
     "c2": c2_dissolution,

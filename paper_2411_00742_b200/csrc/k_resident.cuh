@@ -37,6 +37,15 @@
 
 namespace pbe {
 
+#if PBE_TIMING
+__device__ unsigned long long g_phase_cycles[8];   // sweep, moments+publish, barrier, scalar, steps, [scalar: sums, mass balance, kinetics]
+#define PBE_TSTAMP(v) long long v = clock64()
+#define PBE_TACC(i, a, b) t_acc[i] += (unsigned long long)((b) - (a))   // registers; written at exit
+#else
+#define PBE_TSTAMP(v)
+#define PBE_TACC(i, a, b)
+#endif
+
 // Smem halo: s_halo[(side * V + v) * HS + t + 1], HS = NT + 2, side 0/1 = bins 0/1 of
 // thread t, side 2/3 = bins K-2/K-1 (transposed so a warp's accesses are consecutive).
 // Columns 0 and NT + 1 stay zero: the ghost cells n_{-2} = n_{-1} = n_N = n_{N+1} = 0.
@@ -177,6 +186,9 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
 template <int P, int K, int MAXT, bool CL = false, int MINB = 1>
 __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     namespace cg = cooperative_groups;
+#if PBE_TIMING
+    unsigned long long t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
     constexpr int V = 1 + P;
     constexpr int PP = P > 0 ? P : 1;
     static_assert(K >= 2, "K >= 2");
@@ -310,12 +322,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     // register file to itself; only C, kap, beta and the lane tangents Cdot live across it.
     struct LaneScal {
         D1 c, t, mu3p, dt;
-        double loss, gacc, rms_c, rms_L;
+        double loss, gacc, rms_c, rms_L, tn;       // tn = t_samples[m] (read once per sample)
         long long nstep;
         int m, status, landing;
     };
     // smem copy: primal part once per warp (identical in all lanes), tangent part per lane
-    struct WarpPart { double c, t, mu3p, dt, loss, rms_c, rms_L; long long nstep; int m, status, landing; };
+    struct WarpPart { double c, t, mu3p, dt, loss, rms_c, rms_L, tn; long long nstep; int m, status, landing; };
     struct LanePart { double c, t, mu3p, dt, gacc; };
     WarpPart* s_wp = reinterpret_cast<WarpPart*>(s_halo + 2 * HP);
     LanePart* s_lp = reinterpret_cast<LanePart*>(s_wp + 32);
@@ -324,14 +336,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         const LanePart l = s_lp[tid];
         LaneScal L;
         L.c = mk(w.c, l.c); L.t = mk(w.t, l.t); L.mu3p = mk(w.mu3p, l.mu3p); L.dt = mk(w.dt, l.dt);
-        L.loss = w.loss; L.gacc = l.gacc; L.rms_c = w.rms_c; L.rms_L = w.rms_L;
+        L.loss = w.loss; L.gacc = l.gacc; L.rms_c = w.rms_c; L.rms_L = w.rms_L; L.tn = w.tn;
         L.nstep = w.nstep; L.m = w.m; L.status = w.status; L.landing = w.landing;
         return L;
     };
     auto store_ls = [&](const LaneScal& L) {
         __syncwarp();
         if (lane == 0)
-            s_wp[warp] = WarpPart{L.c.v, L.t.v, L.mu3p.v, L.dt.v, L.loss, L.rms_c, L.rms_L, L.nstep, L.m,
+            s_wp[warp] = WarpPart{L.c.v, L.t.v, L.mu3p.v, L.dt.v, L.loss, L.rms_c, L.rms_L, L.tn, L.nstep, L.m,
                                   L.status, L.landing};
         s_lp[tid] = LanePart{L.c.d, L.t.d, L.mu3p.d, L.dt.d, L.gacc};
     };
@@ -343,13 +355,25 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     const double* tgt = has_target ? kp.target + (size_t)s * kp.M * 2 : nullptr;
     double C = 0.0, kap = 0.0, beta = 0.0, Cd_l = 0.0;
 
-    // kinetics + time step of the next step from scalar state L (row a1, a2)
+    // kinetics + time step of the next step from scalar state L (row a1, a2).  Parameters and this
+    // group's seed rows are staged in shared memory (read by every warp every step).
     const KinCache KC = kin_cache(kp, KL, kT);
-    auto kinetics = [&](LaneScal& L) -> bool {
+    const bool kin_smem = kp.n_params <= MAXTH;
+    const int nsd = kp.n_params + kp.n_sol;
+    __shared__ double s_th[MAXTH], s_sol[3], s_seed[PP * (MAXTH + 3)];
+    if (kin_smem) {
+        const double* th = kp.theta + (size_t)s * kp.n_params;
+        for (int j = tid; j < kp.n_params; j += NT) s_th[j] = th[j];
+        for (int j = tid; j < kp.n_sol; j += NT) s_sol[j] = kp.sol[j];
+        for (int j = tid; j < nl * nsd; j += NT) s_seed[j] = kp.seed[(size_t)lane0 * nsd + j];
+    }
+    __syncthreads();
+    const KinLoaderS KLS{s_th, s_sol, s_seed, pl, kp.n_params, nsd};
+    auto kinetics_with = [&](const auto& LDR, LaneScal& L) -> bool {
         D1 T;
-        const D1 S = supersaturation(kp, KL, kT, KC, L.t, L.c, T);
-        const D1 G = growth_rate(kp, KL, S, T);
-        const double tn = steps_mode ? 0.0 : kp.t_samples[L.m];
+        const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
+        const D1 G = growth_rate(kp, LDR, S, T);
+        const double tn = steps_mode ? 0.0 : L.tn;
         const StepScalars sc = time_step(kp, G, L.t, tn, steps_mode);
         if (sc.err != ST_OK) { L.status = sc.err; return false; }
         L.dt = sc.dt;
@@ -360,6 +384,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         Cd_l = sc.C.d;
         return true;
     };
+    auto kinetics = [&](LaneScal& L) -> bool { return kin_smem ? kinetics_with(KLS, L) : kinetics_with(KL, L); };
 
     bool go = true, sample = false;
     {
@@ -368,10 +393,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         if (CL) {
             for (int r = 0; r < CS; ++r) a += cg::this_cluster().map_shared_rank(&s_cta[1][3][0], r)[0];
         } else {
-            a = sum4(&s_red[1][0][3][0], 4 * V, NW);
+            a = sum4u<(MAXT + 31) / 32>(&s_red[1][0][3][0], 4 * V, NW);
         }
         L.c = mk(kp.c0[s]); L.t = mk(0.0); L.mu3p = mk(a, 0.0); L.dt = mk(0.0);
         L.loss = 0.0; L.gacc = 0.0; L.rms_c = 1.0; L.rms_L = 1.0;
+        L.tn = steps_mode ? 0.0 : kp.t_samples[0];
         L.nstep = 0; L.m = 0; L.status = ST_OK; L.landing = 0;
         if (warp == 0 && has_target) {
             double sc2 = 0.0, sl2 = 0.0;
@@ -394,6 +420,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     while (go) {
         const int q = (int)(n & 1), qp = q ^ 1;
         bool bad;
+        PBE_TSTAMP(tc0);
         const double* hin = s_halo + qp * HP;
         if (MINB == 1) {
             // lane tangents of C in registers
@@ -410,6 +437,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
             if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
             else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
         }
+        PBE_TSTAMP(tc1);
+        PBE_TACC(0, tc0, tc1);
         if (bad) s_bad[q] = n;
         moment_partials(q, std::integral_constant<int, 3>{});     // mu3 of n and every tangent lane
         if (sample) {
@@ -419,7 +448,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         }
         publish_halo(q);
         cta_totals(q, sample);
+        PBE_TSTAMP(tc2);
+        PBE_TACC(1, tc1, tc2);
         block_barrier();                         // the one (cluster) barrier of the step
+        PBE_TSTAMP(tc3);
+        PBE_TACC(2, tc2, tc3);
 
         // ---- scalar phase (every warp, identical arithmetic) -----------------------------
         LaneScal L = load_ls();
@@ -435,12 +468,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
                         if (pl >= 0) b += rc[1 + pl];
                     }
                 } else {
-                    a = sum4(&s_red[q][0][km][0], 4 * V, NW);
-                    if (pl >= 0) b = sum4(&s_red[q][0][km][1 + pl], 4 * V, NW);
+                    a = sum4u<(MAXT + 31) / 32>(&s_red[q][0][km][0], 4 * V, NW);
+                    if (pl >= 0) b = sum4u<(MAXT + 31) / 32>(&s_red[q][0][km][1 + pl], 4 * V, NW);
                 }
                 tot[km] = a; totd[km] = b;
             }
         }
+        PBE_TSTAMP(ts1);
+        PBE_TACC(5, tc3, ts1);
         const D1 mu3n = mk(tot[3], totd[3]);
         const D1 cn = L.c - kp.rho_kv * (mu3n - L.mu3p);        // eq-discrete_mass_balance
         bool any_bad = s_bad[q] == n;
@@ -468,17 +503,28 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
                     L.gacc += 2.0 * (rc / L.rms_c) * L.c.d + 2.0 * (rL / L.rms_L) * Lbd;
                 }
             }
-            if (L.landing) ++L.m;
+            if (L.landing) { ++L.m; if (L.m < kp.M) L.tn = kp.t_samples[L.m]; }
+            PBE_TSTAMP(ts2);
+            PBE_TACC(6, ts1, ts2);
             if (steps_mode ? (L.nstep >= kp.n_steps) : (L.m >= kp.M)) go = false;
             else if (L.nstep >= kp.max_steps) { L.status = ST_MAXSTEPS; go = false; }
             else go = kinetics(L);
+            PBE_TSTAMP(ts3);
+            PBE_TACC(7, ts2, ts3);
         }
         sample = go && (L.landing || (steps_mode && L.nstep + 1 == kp.n_steps));
         store_ls(L);
         ++n;
+        PBE_TSTAMP(tc4);
+        PBE_TACC(3, tc3, tc4);
+        PBE_TACC(4, 0, 1);
     }
 
     // ---- epilogue -----------------------------------------------------------------------
+#if PBE_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int i = 0; i < 8; ++i) g_phase_cycles[i] = t_acc[i];
+#endif
     if (kp.n_final && grp == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) { const int i = i0 + k; if (i < N) kp.n_final[(size_t)s * N + i] = x[0][k]; }

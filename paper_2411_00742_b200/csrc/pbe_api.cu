@@ -564,6 +564,14 @@ extern "C" {
 
 const char* pbe_version(void) { return "libpbe 0.1 (sm_100a)"; }
 
+#if PBE_TIMING
+// Diagnostics build only (tools/build_variant.py ... -DPBE_TIMING=1): cycle sums of the
+// resident kernel's step phases measured by warp 0 of CTA 0.
+int pbe_debug_phase_cycles(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, pbe::g_phase_cycles, sizeof(pbe::g_phase_cycles)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 const char* pbe_last_error(pbe_ctx ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
 
 pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {

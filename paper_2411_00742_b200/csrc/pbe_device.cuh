@@ -132,14 +132,27 @@ struct KinLoader {
     }
 };
 
-__device__ __forceinline__ D1 solubility(const KParams& kp, const KinLoader& L, D1 T) {
+// The same parameters staged in shared memory by the CTA (k_resident: read every step by every
+// warp, so the per-step kinetics sees shared-memory latency instead of L1/L2 latency).
+struct KinLoaderS {
+    const double* th;     // smem [n_params]
+    const double* sol;    // smem [n_sol]
+    const double* seed;   // smem [P][nsd] (rows of this CTA's lane group)
+    int lane_p, n_params, nsd;
+    __device__ __forceinline__ D1 theta(int j) const { return mk(th[j], lane_p >= 0 ? seed[lane_p * nsd + j] : 0.0); }
+    __device__ __forceinline__ D1 so(int j) const { return mk(sol[j], lane_p >= 0 ? seed[lane_p * nsd + n_params + j] : 0.0); }
+};
+
+template <class LD>
+__device__ __forceinline__ D1 solubility(const KParams& kp, const LD& L, D1 T) {
     if (kp.sol_kind == SOL_EXP) return L.so(0) * dexp(L.so(1) * T);          // Eq. A.1
     return L.so(0) + L.so(1) * T + L.so(2) * T * T;                           // R-13
 }
 
 __device__ __forceinline__ D1 dpow(D1 x, D1 y) { return dexp(y * dlog(x)); }   // R-18
 
-__device__ __forceinline__ D1 growth_rate(const KParams& kp, const KinLoader& L, D1 S, D1 T) {
+template <class LD>
+__device__ __forceinline__ D1 growth_rate(const KParams& kp, const LD& L, D1 S, D1 T) {
     if (kp.law == LAW_CONST) return L.theta(0);
     if (kp.law == LAW_ARRH) {
         if (S.v > 1.0)                                                                 // Eq. A.2
@@ -175,7 +188,8 @@ struct KinCache {
     bool const_T;
     D1 T, ics;
 };
-__device__ __forceinline__ KinCache kin_cache(const KParams& kp, const KinLoader& L, const double* kT) {
+template <class LD>
+__device__ __forceinline__ KinCache kin_cache(const KParams& kp, const LD& L, const double* kT) {
     KinCache k;
     k.const_T = (kp.n_knots == 1);
     k.T = mk(kT[0]);
@@ -183,7 +197,8 @@ __device__ __forceinline__ KinCache kin_cache(const KParams& kp, const KinLoader
     return k;
 }
 // S = c / c*(T(t)) (L285) and T
-__device__ __forceinline__ D1 supersaturation(const KParams& kp, const KinLoader& L, const double* kT,
+template <class LD>
+__device__ __forceinline__ D1 supersaturation(const KParams& kp, const LD& L, const double* kT,
                                               const KinCache& kc, D1 t, D1 c, D1& T) {
     if (kc.const_T) { T = kc.T; return c * kc.ics; }
     T = temperature(kp, kT, t);
@@ -193,6 +208,19 @@ __device__ __forceinline__ D1 supersaturation(const KParams& kp, const KinLoader
 // Fixed-order sum of n values base[0], base[stride], ... (n <= 32): four interleaved chains
 // then a pairwise combine — the same order everywhere (deterministic), shorter latency
 // than one sequential chain.
+// The same sum, unrolled up to MAXW terms (identical order and result for n <= MAXW).
+template <int MAXW>
+__device__ __forceinline__ double sum4u(const double* base, int stride, int n) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int w = 0; w < MAXW; w += 4) {
+        if (w < n) a0 += base[w * stride];
+        if (w + 1 < n) a1 += base[(w + 1) * stride];
+        if (w + 2 < n) a2 += base[(w + 2) * stride];
+        if (w + 3 < n) a3 += base[(w + 3) * stride];
+    }
+    return (a0 + a1) + (a2 + a3);
+}
 __device__ __forceinline__ double sum4(const double* base, int stride, int n) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int w = 0; w < n; w += 4) {

@@ -103,7 +103,7 @@ template <class S> inline S sabs(const S& x) {
 // ----------------------------------------------------------------------------------
 // Problem description (the oracle's own struct; NOT shared with include/pbe.h).
 // ----------------------------------------------------------------------------------
-enum { LIM_UPWIND = 0, LIM_VANLEER = 1 };
+enum { LIM_UPWIND = 0, LIM_VANLEER = 1, LIM_MINMOD = 2, LIM_SUPERBEE = 3, LIM_MC = 4 };
 enum { LAW_CONST = 0, LAW_ARRHENIUS = 1, LAW_POLY = 2 };
 enum { SOL_EXP = 0, SOL_POLY = 1 };
 enum { ST_OK = 0, ST_CFL = 2, ST_NEGATIVE = 3, ST_INFEASIBLE = 4, ST_MAXSTEPS = 5 };
@@ -114,7 +114,7 @@ extern "C" {
 typedef struct {
     int32_t N;            // number of bins
     double L_lo, dL;      // bin i has center L_lo + (i + 1/2) dL
-    int32_t limiter;      // 0 upwind (phi = 0), 1 van Leer
+    int32_t limiter;      // 0 upwind (phi = 0), 1 van Leer, 2 minmod, 3 superbee, 4 MC
     double courant;       // nu (0.9)
     double dt_fixed;      // > 0: fixed time step; 0: CFL time step
     double dt_max;        // cap on the CFL time step (INFINITY = paper behaviour)
@@ -187,14 +187,29 @@ template <class S> S growth_rate(const oracle_problem& pb, const S* th, const S&
 // FVM update (rows a3, a4): eq-highRes_growth written out literally for C >= 0.
 // Ghost cells f_{-2} = f_{-1} = f_N = f_{N+1} = 0 (boundary conditions L278-280, R-25).
 // ----------------------------------------------------------------------------------
+// min / max on the real part; the result (value and derivative) is the chosen argument,
+// ties take the second argument.
+template <class S> S smin(const S& x, const S& y) { return re(x) < re(y) ? x : y; }
+template <class S> S smax(const S& x, const S& y) { return re(x) > re(y) ? x : y; }
+
 // phi(theta) * den with theta = num/den (SI L851, L855).  den == 0 -> 0 (R-4).
+// van Leer (SI L855) is the paper's limiter (L299-300).  NEXT-4 adds three classical Sweby-region
+// limiters in the same phi(theta) form (R-31; every one is 0 for theta <= 0):
+//   minmod    phi = max(0, min(1, theta))
+//   superbee  phi = max(0, min(2 theta, 1), min(theta, 2))
+//   MC        phi = max(0, min(2 theta, (1 + theta)/2, 2))
 template <class S> S phi_times_den(const S& num, const S& den, int limiter) {
     if (limiter == LIM_UPWIND) return S(0.0);   // first-order upwind: phi = 0 (R-5)
     if (re(den) == 0.0) return S(0.0);
     const S theta = num / den;
-    if (!(re(theta) > 0.0)) return S(0.0);      // (theta + |theta|) = 0 for theta <= 0
-    if (std::isinf(re(theta))) return S(2.0) * den;  // lim phi = 2
-    const S phi = (theta + sabs(theta)) / (1.0 + sabs(theta));
+    if (!(re(theta) > 0.0)) return S(0.0);      // every limiter is 0 for theta <= 0
+    if (std::isinf(re(theta)))                   // lim_{theta -> inf} phi
+        return (limiter == LIM_MINMOD ? S(1.0) : S(2.0)) * den;
+    S phi;
+    if (limiter == LIM_VANLEER) phi = (theta + sabs(theta)) / (1.0 + sabs(theta));
+    else if (limiter == LIM_MINMOD) phi = smin(S(1.0), theta);
+    else if (limiter == LIM_SUPERBEE) phi = smax(smin(2.0 * theta, S(1.0)), smin(theta, S(2.0)));
+    else phi = smin(smin(2.0 * theta, (1.0 + theta) * 0.5), S(2.0));   // MC
     return phi * den;
 }
 

@@ -23,7 +23,7 @@ __all__ = ["PBEError", "Context", "run_workload", "lib_path", "load_library", "E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
-LIM_UPWIND, LIM_VANLEER = 0, 1
+LIM_UPWIND, LIM_VANLEER, LIM_MINMOD, LIM_SUPERBEE, LIM_MC = 0, 1, 2, 3, 4
 LAW_CONST, LAW_ARRHENIUS_GD, LAW_POLY = 0, 1, 2
 SOL_EXP, SOL_POLY = 0, 1
 KERNEL_AUTO, KERNEL_RESIDENT, KERNEL_CLUSTER, KERNEL_STREAM, KERNEL_2D, KERNEL_ADJOINT = 0, 1, 2, 3, 4, 5

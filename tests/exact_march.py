@@ -46,7 +46,21 @@ class Num:
 def psi(a, b, limiter):
     if limiter == 0:
         return 0
-    return 2 * a * b / (a + b) if a * b > 0 else 0
+    if not a * b > 0:
+        return 0
+    if limiter == 1:
+        return 2 * a * b / (a + b)
+    # NEXT-4 limiters as slope limiters on |a|, |b| with the sign of b (R-31): minmod,
+    # superbee, MC (Sweby's region; LeVeque, "Finite Volume Methods", eqs. 6.39-6.44)
+    A, B = abs(a), abs(b)
+    sgn = 1 if b > 0 else -1
+    if limiter == 2:
+        m = min(A, B)
+    elif limiter == 3:
+        m = max(min(2 * A, B), min(A, 2 * B))
+    else:
+        m = min(2 * A, (A + B) / 2, 2 * B)
+    return sgn * m
 
 
 def flux_step(n, Cn, limiter):

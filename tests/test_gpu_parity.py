@@ -117,6 +117,17 @@ def test_c5_tangents_small():
     assert np.allclose(g["grad"], go, rtol=1e-8, atol=1e-9 * np.max(np.abs(go)))
 
 
+@pytest.mark.parametrize("kernel", [0, 3])
+def test_lognormal_seed_matches_oracle(kernel):
+    """Log-normal seed through the resident (AUTO) and streaming kernels,
+    with tangents."""
+    w = W.c5_ensemble(n_sims=9, N=300, t_max=40.0, M=40, n_tangents=4 if kernel == 3 else 8)
+    w = W.replace(w, n0=W.lognormal_seed(300, w.dL, mean=380.0, sigma=45.0)[None, :])
+    g, o = _check(w, mode=oracle.MODE_DUAL, kernel=kernel)
+    lo, go = oracle.loss_and_grad(o["samples"], o["tsamples"], w.target)
+    assert np.allclose(g["loss"], lo, rtol=1e-9, atol=0)
+
+
 def test_c5_full_size_sampled_sims():
     """C5 exactly as bench.py runs it (4096 sims x 2000 bins, 8 tangents) — oracle on 2 sims."""
     w = W.c5_ensemble()

@@ -135,19 +135,39 @@ def _rand_profile(rng, N):
     return f
 
 
-@pytest.mark.parametrize("lim", [W.LIM_UPWIND, W.LIM_VANLEER])
+ALL_LIMS = [W.LIM_UPWIND, W.LIM_VANLEER, W.LIM_MINMOD, W.LIM_SUPERBEE, W.LIM_MC]
+
+
+@pytest.mark.parametrize("lim", ALL_LIMS)
 def test_pin3_zero_courant_is_identity(lim):
     f = _rand_profile(np.random.default_rng(1), 40)
     assert np.array_equal(oracle.sweep(f, 0.0, lim), f)
 
 
-@pytest.mark.parametrize("lim", [W.LIM_UPWIND, W.LIM_VANLEER])
+@pytest.mark.parametrize("lim", ALL_LIMS)
 def test_pin4_courant_one_is_exact_shift(lim):
     f = _rand_profile(np.random.default_rng(2), 50)
     out = oracle.sweep(f, 1.0, lim)
     assert np.array_equal(out[1:], f[:-1]) and out[0] == 0.0
     out = oracle.sweep(f, -1.0, lim)
     assert np.array_equal(out[:-1], f[1:]) and out[-1] == 0.0
+
+
+@pytest.mark.parametrize("lim", [W.LIM_MINMOD, W.LIM_SUPERBEE, W.LIM_MC])
+def test_pin2_extra_limiters_phi_values(lim):
+    """phi(theta) of the NEXT-4 limiters at closed-form points, read off one face: with
+    f = (0, 0, p, p + 1, 0...) the face between bins 2 and 3 has d_2 = p, d_3 = 1, i.e.
+    theta = p, and the flux difference isolates phi(p) (C = 1/2, kappa = 1/8)."""
+    table = {W.LIM_MINMOD: {0.25: 0.25, 0.5: 0.5, 1.0: 1.0, 2.0: 1.0, 3.0: 1.0},
+             W.LIM_SUPERBEE: {0.25: 0.5, 0.5: 1.0, 1.0: 1.0, 1.5: 1.5, 2.0: 2.0, 3.0: 2.0},
+             W.LIM_MC: {0.25: 0.5, 0.5: 0.75, 1.0: 1.0, 2.0: 1.5, 3.0: 2.0}}[lim]
+    for p, phi in table.items():
+        f = np.array([0.0, 0.0, p, p + 1.0, 0.0, 0.0, 0.0])
+        up = oracle.sweep(f, 0.5, W.LIM_UPWIND)
+        out = oracle.sweep(f, 0.5, lim)
+        # bin 3 gains F_{3-1/2} - F_{3+1/2}; the limited part of F_{3-1/2} is kappa phi(p) * 1
+        # and F_{3+1/2} has theta = 1/(-(p+1)) < 0 -> no limited part
+        assert (out[3] - up[3]) == pytest.approx(0.125 * phi, rel=1e-14, abs=1e-15), (p, phi)
 
 
 def test_pin2_vanleer_values_through_sweep():
@@ -167,29 +187,33 @@ def test_pin9_sweep_matches_exact_flux_form(seed):
     N = 10
     f = [Fraction(int(x), 7) for x in rng.integers(0, 50, N)]
     C = Fraction(int(rng.integers(-9, 10)), 10)
-    for lim in (0, 1):
+    for lim in (0, 1, 2, 3, 4):
         exact = X.flux_step(f, C, lim)
         got = oracle.sweep(np.array([float(x) for x in f]), float(C), lim)
         scale = float(max(f)) or 1.0
         assert np.max(np.abs(got - np.array([float(x) for x in exact]))) <= 1e-15 * scale
 
 
+@pytest.mark.parametrize("lim", ALL_LIMS[1:])
 @pytest.mark.parametrize("seed", range(10))
-def test_pin6_mirror_identity(seed):
+def test_pin6_mirror_identity(seed, lim):
     rng = np.random.default_rng(200 + seed)
     f = _rand_profile(rng, 30)
     C = float(rng.uniform(0, 1))
-    a = oracle.sweep(f, -C, W.LIM_VANLEER)
-    b = oracle.sweep(f[::-1].copy(), C, W.LIM_VANLEER)[::-1]
+    a = oracle.sweep(f, -C, lim)
+    b = oracle.sweep(f[::-1].copy(), C, lim)[::-1]
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("lim", ALL_LIMS[1:])
 @pytest.mark.parametrize("seed", range(30))
-def test_pin8_positivity_and_tvd(seed):
+def test_pin8_positivity_and_tvd(seed, lim):
+    """All limiters lie in Sweby's TVD region (0 <= phi <= min(2 theta, 2)), so the sweep is
+    positivity preserving and total-variation diminishing for |C| <= 1."""
     rng = np.random.default_rng(300 + seed)
     f = _rand_profile(rng, 64) * 10.0 ** rng.uniform(-5, 5)
     C = float(rng.uniform(-1, 1))
-    out = oracle.sweep(f, C, W.LIM_VANLEER)
+    out = oracle.sweep(f, C, lim)
     tv = lambda v: np.sum(np.abs(np.diff(np.concatenate([[0, 0], v, [0, 0]]))))
     assert out.min() >= -1e-12 * f.max()
     assert tv(out) <= tv(f) * (1 + 1e-12)
@@ -328,6 +352,24 @@ def test_pin10_seed_moments(N):
     assert W.RHO_C * W.K_V * mu[3] == pytest.approx(1.0, rel=1e-14)
 
 
+@pytest.mark.parametrize("N,mean,sigma", [(1000, 400.0, 30.0), (2000, 300.0, 40.0)])   # tails beyond 1200 um < 1e-20
+def test_pin10_lognormal_seed_moments(N, mean, sigma):
+    """Log-normal seed (L882-883): the discrete moments are the log-normal raw moments
+    E[L^k] = exp(k mu_l + k^2 s_l^2 / 2), with mean and std of L as given."""
+    dL = 1200.0 / N
+    n0 = W.lognormal_seed(N, dL, mean=mean, sigma=sigma)
+    w = W.replace(W.c4_sweep(N), n0=n0[None, :])
+    mu = oracle.moments(w, n0)
+    s2 = math.log1p((sigma / mean) ** 2)
+    ml = math.log(mean) - 0.5 * s2
+    raw = [math.exp(k * ml + 0.5 * k * k * s2) for k in range(4)]
+    assert mu[1] / mu[0] == pytest.approx(mean, rel=1e-13)
+    assert mu[2] / mu[0] - (mu[1] / mu[0]) ** 2 == pytest.approx(sigma ** 2, rel=1e-9)
+    for k in (2, 3):
+        assert mu[k] / mu[0] == pytest.approx(raw[k], rel=1e-13)
+    assert W.RHO_C * W.K_V * mu[3] == pytest.approx(1.0, rel=1e-13)
+
+
 # ------------------------------------------------------------------------------------
 # PIN-11 / PIN-13: constant-G exact translation n(L, t) = n0(L - G t); van Leer is
 # second order away from extrema, upwind first order
@@ -421,6 +463,18 @@ def test_pin14_dual_equals_complex_step():
             if k == 1:      # d mu0: zero up to rounding (no boundary flux)
                 continue
             assert np.max(np.abs(a[:, k] - b[:, k])) <= 1e-12 * scale
+        sa = np.max(np.abs(rd["ndot_final"][0, p])); assert sa > 0
+        assert np.max(np.abs(rd["ndot_final"][0, p] - rc["ndot_final"][0, p])) <= 1e-11 * sa
+
+
+@pytest.mark.parametrize("lim", [W.LIM_MINMOD, W.LIM_SUPERBEE, W.LIM_MC])
+def test_pin14_dual_equals_complex_step_extra_limiters(lim):
+    """The piecewise-linear limiters' dual arithmetic (branch derivatives) equals complex-step."""
+    w = W.replace(_tangent_case(), limiter=lim)
+    rd = oracle.run(w, mode=oracle.MODE_DUAL)
+    rc = oracle.run(w, mode=oracle.MODE_CSTEP)
+    assert np.array_equal(rd["samples"], rc["samples"])
+    for p in range(w.n_tangents):
         sa = np.max(np.abs(rd["ndot_final"][0, p])); assert sa > 0
         assert np.max(np.abs(rd["ndot_final"][0, p] - rc["ndot_final"][0, p])) <= 1e-11 * sa
 

@@ -23,7 +23,7 @@ from typing import Optional
 import numpy as np
 
 # enums (values mirror include/pbe.h; the oracle has its own copy of these small ints)
-LIM_UPWIND, LIM_VANLEER = 0, 1
+LIM_UPWIND, LIM_VANLEER, LIM_MINMOD, LIM_SUPERBEE, LIM_MC = 0, 1, 2, 3, 4
 LAW_CONST, LAW_ARRHENIUS, LAW_POLY = 0, 1, 2
 SOL_EXP, SOL_POLY = 0, 1
 
@@ -117,6 +117,25 @@ def gaussian_seed(N: int, dL: float, mean: float = 400.0, sigma: float = 30.0, m
     L = bin_centers(N, dL, L_lo)
     Nc = m0 / (rho_c * k_v * (mean ** 3 + 3.0 * mean * sigma ** 2))
     return Nc * np.exp(-0.5 * ((L - mean) / sigma) ** 2) / (sigma * math.sqrt(2.0 * math.pi))
+
+
+def lognormal_seed(N: int, dL: float, mean: float = 400.0, sigma: float = 30.0, m0: float = 1.0,
+                   L_lo: float = 0.0, rho_c: float = RHO_C, k_v: float = K_V) -> np.ndarray:
+    """Log-normal number density at bin centers with the given mean and standard deviation of
+    L ("Our framework supports normal and log-normal distributions for the
+    seed PSSD"): ln L ~ N(mu_l, s_l^2), s_l^2 = ln(1 + sigma^2/mean^2), mu_l = ln(mean) - s_l^2/2,
+    raw moments E[L^k] = exp(k mu_l + k^2 s_l^2 / 2); scaled analytically to crystal mass
+    rho_c k_v E[L^3] N_c = m0 like gaussian_seed."""
+    L = bin_centers(N, dL, L_lo)
+    s2 = math.log1p((sigma / mean) ** 2)
+    mu = math.log(mean) - 0.5 * s2
+    EL3 = math.exp(3.0 * mu + 4.5 * s2)
+    Nc = m0 / (rho_c * k_v * EL3)
+    out = np.zeros(N)
+    pos = L > 0.0
+    Lp = L[pos]
+    out[pos] = Nc * np.exp(-0.5 * (np.log(Lp) - mu) ** 2 / s2) / (Lp * math.sqrt(2.0 * math.pi * s2))
+    return out
 
 
 def _target(c0: np.ndarray, t: np.ndarray, L0: float = 400.0) -> np.ndarray:

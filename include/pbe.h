@@ -58,7 +58,8 @@ typedef enum {
     PBE_ERR_STATE = 8        /* call out of order (e.g. run before set_kinetics) */
 } pbe_status;
 
-enum { PBE_LIM_UPWIND = 0, PBE_LIM_VANLEER = 1 };          /* phi = 0 / van Leer (SI L855) */
+enum { PBE_LIM_UPWIND = 0, PBE_LIM_VANLEER = 1,         /* phi = 0 / van Leer (SI L855), the paper's */
+       PBE_LIM_MINMOD = 2, PBE_LIM_SUPERBEE = 3, PBE_LIM_MC = 4 };  /* NEXT-4 extras (R-31) */
 enum {
     PBE_LAW_CONST = 0,         /* G = theta0 (size- and S-independent; config C1)         */
     PBE_LAW_ARRHENIUS_GD = 1,  /* theta = (kg, Eg, g[, kd, Ed, d]): Eq. A.2 for S > 1;   */
@@ -80,7 +81,7 @@ typedef struct {
     int32_t n_bins;      /* N >= 3 */
     double  L_lo;        /* bin i has center L_lo + (i + 1/2) dL (R-2) */
     double  dL;          /* > 0 */
-    int32_t limiter;     /* PBE_LIM_* */
+    int32_t limiter;     /* PBE_LIM_*: phi(theta) of eq-highRes_growth; van Leer in the paper (L299-300) */
     double  courant;     /* nu in (0, 1]; the paper uses 0.9 (L301) */
     double  dt_fixed;    /* > 0: fixed-dt mode (|C| <= 1 checked per step); 0: CFL mode */
     double  dt_max;      /* CFL cap (> 0); INFINITY = the paper's uncapped CFL step */

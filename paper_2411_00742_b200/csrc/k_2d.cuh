@@ -47,7 +47,7 @@ struct Params2D {
 
 // Update K consecutive cells of one line (window w[0..K+3] = cells -2 .. K+1) with Courant C.
 template <bool NEG>
-__device__ __forceinline__ void line_update(const double (&w)[K2D_K + 4], double C, double kap2, bool vl,
+__device__ __forceinline__ void line_update(const double (&w)[K2D_K + 4], double C, double kap2, int lim,
                                             double (&y)[K2D_K]) {
     double F[K2D_K + 1];
 #pragma unroll
@@ -55,7 +55,7 @@ __device__ __forceinline__ void line_update(const double (&w)[K2D_K + 4], double
         const int u = NEG ? f : f - 1;
         const int ja = NEG ? f + 1 : f - 1;
         const double a = w[ja] - w[ja - 1], b = w[f] - w[f - 1];
-        const double h = vl ? psi_vl(a, b) * 0.5 : 0.0;
+        const double h = psi_half(lim, a, b);
         F[f - 2] = fma(C, w[u], kap2 * h);
     }
 #pragma unroll
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(K2D_NT, 3) k_2d(const Params2D p2) {
     const int S = kp.n_sims, N1 = kp.N, N2 = p2.N2;
     const long long P1 = p2.P1, PL = p2.R2 * P1;                   // plane size
     const bool steps_mode = kp.n_steps > 0;
-    const bool vl = kp.limiter == LIM_VANLEER;
+    const int vl = kp.limiter;                 // limiter (name kept: van Leer is the paper's)
     const int H = kp.n_params / 2;
 
     // per-simulation coefficients of the current step + scalar state (identical in all CTAs)

@@ -69,6 +69,14 @@ __device__ __forceinline__ double limited(double a, double b, double k2h) {   //
     return (k2h * num) * rcp_nr(den);
 }
 
+// Limited term of a face: van Leer / upwind use the select-free form above (k = k2/2 or 0);
+// GEN (minmod, superbee, MC; NEXT-4) goes through psi_half with k = k2 = 2 kap.
+template <bool GEN>
+__device__ __forceinline__ double lim_term(double a, double b, double k, int lim) {
+    if (GEN) return k * psi_half(lim, a, b);
+    return limited(a, b, k);
+}
+
 // Sliding state of one lane's column for sweep 2.
 struct ColState {
     double gm3, gm2, gm1, Fprev;     // g of rows r-3, r-2, r-1; face below row r-3
@@ -79,23 +87,24 @@ struct ColState {
 
 // One input row of a strip: sweep 1 across lanes, then the sweep-2 face between rows r-2 and
 // r-1; if EMIT, the finished cell of row r-2 is clipped, stored and added to the moments.
-template <bool NEG1, bool NEG2, bool EMIT>
+template <bool NEG1, bool NEG2, bool EMIT, bool GEN>
 __device__ __forceinline__ void strip_row(double w, ColState& cs, double C1, double k1, double C2, double k2,
-                                          double clip, double dL2, bool own, bool ok, bool sample, double* dst) {
+                                          double clip, double dL2, bool own, bool ok, bool sample, double* dst,
+                                          int lim) {
     const double wm1 = __shfl_up_sync(0xffffffffu, w, 1);
     double F;
     if (!NEG1) {
         const double wm2 = __shfl_up_sync(0xffffffffu, w, 2);
-        F = fma(C1, wm1, limited(wm1 - wm2, w - wm1, k1));
+        F = fma(C1, wm1, lim_term<GEN>(wm1 - wm2, w - wm1, k1, lim));
     } else {
         const double wp1 = __shfl_down_sync(0xffffffffu, w, 1);
-        F = fma(C1, w, limited(wp1 - w, w - wm1, k1));
+        F = fma(C1, w, lim_term<GEN>(wp1 - w, w - wm1, k1, lim));
     }
     const double Fp = __shfl_down_sync(0xffffffffu, F, 1);
     const double g = w - (Fp - F);                 // ghost rows: w = 0 in all lanes -> g = 0
     double F2;
-    if (!NEG2) F2 = fma(C2, cs.gm2, limited(cs.gm2 - cs.gm3, cs.gm1 - cs.gm2, k2));
-    else       F2 = fma(C2, cs.gm1, limited(g - cs.gm1, cs.gm1 - cs.gm2, k2));
+    if (!NEG2) F2 = fma(C2, cs.gm2, lim_term<GEN>(cs.gm2 - cs.gm3, cs.gm1 - cs.gm2, k2, lim));
+    else       F2 = fma(C2, cs.gm1, lim_term<GEN>(g - cs.gm1, cs.gm1 - cs.gm2, k2, lim));
     if (EMIT) {                                    // ok: row r-2 < N2 (no branch: keeps the warp converged)
         const bool keep = own && ok;
         double v = cs.gm2 - (F2 - cs.Fprev);
@@ -114,10 +123,10 @@ __device__ __forceinline__ void strip_row(double w, ColState& cs, double C1, dou
 // One warp strip: march rows j0-2 .. j0+H+1 of fin (RB-row load batches, ping-pong prefetch),
 // write the owned cells of rows j0 .. j0+H-1 to fout.  Per-lane moment sums in cs (the caller
 // applies the column weights and drops the halo lanes).
-template <bool NEG1, bool NEG2>
+template <bool NEG1, bool NEG2, bool GEN>
 __device__ __forceinline__ void strip_march(const double* __restrict__ fin, double* __restrict__ fout, long long P1,
                                             int N1, int N2, int is, int j0, double C1, double k1, double C2, double k2,
-                                            double clip, bool sample, double dL2, double L2_lo, ColState& cs) {
+                                            double clip, bool sample, double dL2, double L2_lo, ColState& cs, int lim) {
     constexpr int RB = F2_RB, NB = (F2_H + 4) / F2_RB;
     static_assert((F2_H + 4) % F2_RB == 0 && NB % 2 == 1 && RB >= 4, "batch layout");
     const int lane = threadIdx.x & 31;
@@ -135,10 +144,10 @@ __device__ __forceinline__ void strip_march(const double* __restrict__ fin, doub
     for (int q = 0; q < RB; ++q) B[q] = src[(size_t)(RB + q) * P1];
     // batch 0: rows 0..3 fill the window, rows 4..RB-1 emit rows j0 .. j0+RB-5
 #pragma unroll
-    for (int q = 0; q < 4; ++q) strip_row<NEG1, NEG2, false>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, true, sample, dst);
+    for (int q = 0; q < 4; ++q) strip_row<NEG1, NEG2, false, GEN>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, true, sample, dst, lim);
 #pragma unroll
     for (int q = 4; q < RB; ++q) {
-        strip_row<NEG1, NEG2, true>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, q - 4 < nrow, sample, dst);
+        strip_row<NEG1, NEG2, true, GEN>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, q - 4 < nrow, sample, dst, lim);
         dst += P1;
     }
 #pragma unroll
@@ -148,7 +157,7 @@ __device__ __forceinline__ void strip_march(const double* __restrict__ fin, doub
     for (int k = 1; k < NB; k += 2) {
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
-            strip_row<NEG1, NEG2, true>(B[q], cs, C1, k1, C2, k2, clip, dL2, own, e + q < nrow, sample, dst);
+            strip_row<NEG1, NEG2, true, GEN>(B[q], cs, C1, k1, C2, k2, clip, dL2, own, e + q < nrow, sample, dst, lim);
             dst += P1;
         }
         if (k + 2 < NB) {
@@ -157,7 +166,7 @@ __device__ __forceinline__ void strip_march(const double* __restrict__ fin, doub
         }
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
-            strip_row<NEG1, NEG2, true>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, e + RB + q < nrow, sample, dst);
+            strip_row<NEG1, NEG2, true, GEN>(A[q], cs, C1, k1, C2, k2, clip, dL2, own, e + RB + q < nrow, sample, dst, lim);
             dst += P1;
         }
         if (k + 3 < NB) {
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(F2_NT, PBE_F2_MINB) k_2d_fused(const Params2DF
     const int S = kp.n_sims, N1 = kp.N, N2 = p.N2;
     const long long P1 = p.P1, PL = p.R2 * P1;
     const bool steps_mode = kp.n_steps > 0;
-    const bool vl = kp.limiter == LIM_VANLEER;
+    const int lim = kp.limiter;
     const int H = kp.n_params / 2;
     const int T2 = p.NTX * p.NTY;
 
@@ -283,14 +292,23 @@ __global__ void __launch_bounds__(F2_NT, PBE_F2_MINB) k_2d_fused(const Params2DF
                 ColState cs;
                 cs.S0 = cs.S1 = cs.S2 = 0.0;
                 cs.bad = false;
-                const double k1v = vl ? 0.5 * k1 : 0.0, k2v = vl ? 0.5 * k2 : 0.0;   // k2/2; upwind: no limited term
-                const int sel = (C1 < 0.0 ? 2 : 0) + (C2 < 0.0 ? 1 : 0);
-#define PBE_STRIP(A, B) strip_march<A, B>(fi, fo, P1, N1, N2, is, j0, C1, k1v, C2, k2v, clip, sample, p.dL2, p.L2_lo, cs)
+                // van Leer: k2/2 into the select-free form; upwind: no limited term; other
+                // limiters (NEXT-4): the generic path with the full k2
+                const bool gen = lim != LIM_VANLEER && lim != LIM_UPWIND;
+                const double k1v = gen ? k1 : (lim == LIM_VANLEER ? 0.5 * k1 : 0.0);
+                const double k2v = gen ? k2 : (lim == LIM_VANLEER ? 0.5 * k2 : 0.0);
+                const int sel = (gen ? 4 : 0) + (C1 < 0.0 ? 2 : 0) + (C2 < 0.0 ? 1 : 0);
+#define PBE_STRIP(A, B, GG) strip_march<A, B, GG>(fi, fo, P1, N1, N2, is, j0, C1, k1v, C2, k2v, clip, sample, p.dL2, \
+                                                  p.L2_lo, cs, lim)
                 switch (sel) {
-                    case 0: PBE_STRIP(false, false); break;
-                    case 1: PBE_STRIP(false, true); break;
-                    case 2: PBE_STRIP(true, false); break;
-                    default: PBE_STRIP(true, true); break;
+                    case 0: PBE_STRIP(false, false, false); break;
+                    case 1: PBE_STRIP(false, true, false); break;
+                    case 2: PBE_STRIP(true, false, false); break;
+                    case 3: PBE_STRIP(true, true, false); break;
+                    case 4: PBE_STRIP(false, false, true); break;
+                    case 5: PBE_STRIP(false, true, true); break;
+                    case 6: PBE_STRIP(true, false, true); break;
+                    default: PBE_STRIP(true, true, true); break;
                 }
 #undef PBE_STRIP
                 bad = cs.bad;

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const int NT = blockDim.x, NW = NT >> 5;
     const int N = kp.N, NP = NT * K + 4;
     const int i0 = tid * K;
-    const bool vl = kp.limiter == LIM_VANLEER;
+    const int lim = kp.limiter;
     const double rho = kp.rho_kv;
     const int Kseg = ap.Kseg;
     double* trs = ap.tr + (size_t)s * kp.max_steps * ADJ_TR;
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
 #pragma unroll
         for (int f = 0; f <= K; ++f) {                             // face between bins i0+f-1 | i0+f
             if (C >= 0.0) {
-                const double h = vl ? 0.5 * psi_vl(w[f + 1] - w[f], w[f + 2] - w[f + 1]) : 0.0;
+                const double h = psi_half(lim, w[f + 1] - w[f], w[f + 2] - w[f + 1]);
                 F[f] = fma(C, w[f + 1], kap2 * h);
             } else {
-                const double h = vl ? 0.5 * psi_vl(w[f + 3] - w[f + 2], w[f + 2] - w[f + 1]) : 0.0;
+                const double h = psi_half(lim, w[f + 3] - w[f + 2], w[f + 2] - w[f + 1]);
                 F[f] = fma(C, w[f + 2], kap2 * h);
             }
         }
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                     a = w[e + 2] - w[e + 1]; b = w[e + 1] - w[e]; nup = w[e + 1];
                 }
                 double h = 0.0, qa = 0.0, qb = 0.0;
-                if (vl) psi_half_d(a, b, h, qa, qb);
+                psi_half_dl(lim, a, b, h, qa, qb);
                 const double pak = kap2 * qa, pbk = kap2 * qb;
                 if (C >= 0.0) { whi[e] = pbk; wmid[e] = C + (pak - pbk); wlo[e] = -pak; }
                 else          { whi[e] = pak; wmid[e] = C - (pak - pbk); wlo[e] = -pbk; }

@@ -49,10 +49,10 @@ __device__ unsigned long long g_phase_cycles[8];   // sweep, moments+publish, ba
 // Smem halo: s_halo[(side * V + v) * HS + t + 1], HS = NT + 2, side 0/1 = bins 0/1 of
 // thread t, side 2/3 = bins K-2/K-1 (transposed so a warp's accesses are consecutive).
 // Columns 0 and NT + 1 stay zero: the ghost cells n_{-2} = n_{-1} = n_N = n_{N+1} = 0.
-template <int P, int K, bool NEG, class CdT>
+template <int P, int K, bool NEG, bool GEN, class CdT>
 __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* __restrict__ s_halo,
                                            int NT, int tid, double C, double kap, double beta,
-                                           const CdT& Cd, bool vl, int i0, int N,
+                                           const CdT& Cd, int lim, int i0, int N,
                                            double clip_thr) {
     constexpr int V = 1 + P;
     bool bad = false;
@@ -84,7 +84,8 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
         const int ja = NEG ? f + 1 : f - 1;
         const double a = X(0, ja) - X(0, ja - 1), b = X(0, f) - X(0, f - 1);
         double h = 0.0, qa = 0.0, qb = 0.0;          // psi = 2h, d psi/da = 2qa, d psi/db = 2qb
-        if (vl) psi_half_d(a, b, h, qa, qb);
+        if (GEN) psi_half_other(lim, a, b, h, qa, qb);        // minmod / superbee / MC (NEXT-4)
+        else if (lim == LIM_VANLEER) psi_half_d(a, b, h, qa, qb);
         const double nup = X(0, u);
         FaceP r;
         r.F = fma(C, nup, kap2 * h);                   // C n_up + kap psi
@@ -415,7 +416,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         store_ls(L);
     }
 
-    const bool vl = kp.limiter == LIM_VANLEER;
+    const int vl = kp.limiter;                                  // limiter id
+    const bool gen = vl != LIM_VANLEER && vl != LIM_UPWIND;      // NEXT-4 limiters: generic sweep
     long long n = 0;
     while (go) {
         const int q = (int)(n & 1), qp = q ^ 1;
@@ -427,15 +429,25 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
             double Cd[PP];
 #pragma unroll
             for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? __shfl_sync(0xffffffffu, Cd_l, p) : 0.0;
-            if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
-            else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+            if (!gen) {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+            } else {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+            }
         } else {
             // 2 CTAs/SM (<= 128 registers): lane tangents of C re-read from this warp's smem slot
             volatile double* cdw = s_cdw + warp * PP;
             if (lane < PP) cdw[lane] = Cd_l;
             __syncwarp();
-            if (C >= 0.0) bad = sweep_bins<P, K, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
-            else          bad = sweep_bins<P, K, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+            if (!gen) {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+            } else {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+            }
         }
         PBE_TSTAMP(tc1);
         PBE_TACC(0, tc0, tc1);
@@ -468,8 +480,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
                         if (pl >= 0) b += rc[1 + pl];
                     }
                 } else {
-                    a = sum4u<(MAXT + 31) / 32>(&s_red[q][0][km][0], 4 * V, NW);
-                    if (pl >= 0) b = sum4u<(MAXT + 31) / 32>(&s_red[q][0][km][1 + pl], 4 * V, NW);
+                    // lane v < V sums component v over the warps (fixed order, sum4u), then the
+                    // primal total and this lane's tangent total are broadcast by shuffles
+                    const double tv = lane < V ? sum4u<(MAXT + 31) / 32>(&s_red[q][0][km][lane], 4 * V, NW) : 0.0;
+                    a = __shfl_sync(0xffffffffu, tv, 0);
+                    b = __shfl_sync(0xffffffffu, tv, pl >= 0 ? 1 + pl : 0);
+                    if (pl < 0) b = 0.0;
                 }
                 tot[km] = a; totd[km] = b;
             }

@@ -122,7 +122,7 @@ struct SimCoef {
 // partials, 16-byte stores.  NEG = (C < 0) (direction is uniform per tile).
 template <int P, int K, bool NEG>
 __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int RS, int g0, int nb, int i_base,
-                                            const SimCoef<P>& cf, bool vl, bool sample, double L_half, double dL,
+                                            const SimCoef<P>& cf, int lim, bool sample, double L_half, double dL,
                                             double* __restrict__ drow, long long pitch,
                                             double (&acc)[4][1 + P], bool& neg) {
     constexpr int V = 1 + P;
@@ -143,7 +143,7 @@ __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int R
         const int ja = NEG ? f + 1 : f - 1;
         const double a = x[0][ja] - x[0][ja - 1], b = x[0][f] - x[0][f - 1];
         double h = 0.0, qa = 0.0, qb = 0.0;
-        if (vl) psi_half_d(a, b, h, qa, qb);
+        psi_half_dl(lim, a, b, h, qa, qb);
         const double nup = x[0][u];
         F[f - 2] = fma(C, nup, kap2 * h);
         if (P > 0) {
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
     long long n = 0;
     int src_sel = 0;
     unsigned long long qq = 0;          // running tile counter (stage = qq % STG, phase = (qq / STG) & 1)
-    const bool vl = kp.limiter == LIM_VANLEER;
+    const int vl = kp.limiter;
     auto tile_active = [&](long long t) { return s_coef[(int)(t / sp.T_sim) - s_lo].active != 0; };
     auto next_active = [&](long long t) { while (t < t_hi && !tile_active(t)) ++t; return t; };
     while (true) {

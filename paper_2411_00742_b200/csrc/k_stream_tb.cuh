@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(TB_NT, 2) k_stream_tb(const StreamTBParams sp)
     const int N = kp.N, TB = sp.TB;
     const int WL = TB + 2 * GH;                       // window length (cells)
     const unsigned G = gridDim.x;
-    const bool vl = kp.limiter == LIM_VANLEER;
+    const int vl = kp.limiter;
     const double L_half = kp.L_lo + 0.5 * kp.dL;
 
     const long long t_lo = (sp.n_tiles * blockIdx.x) / G;

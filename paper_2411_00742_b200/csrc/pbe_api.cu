@@ -581,7 +581,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (c.n_bins < 3) return fail(nullptr, PBE_ERR_ARG, "n_bins must be >= 3 (got %d)", c.n_bins);
     if (!(c.dL > 0.0) || !std::isfinite(c.dL)) return fail(nullptr, PBE_ERR_ARG, "dL must be finite and > 0");
     if (!std::isfinite(c.L_lo)) return fail(nullptr, PBE_ERR_ARG, "L_lo must be finite");
-    if (c.limiter != PBE_LIM_UPWIND && c.limiter != PBE_LIM_VANLEER)
+    if (c.limiter < PBE_LIM_UPWIND || c.limiter > PBE_LIM_MC)
         return fail(nullptr, PBE_ERR_ARG, "unknown limiter %d", c.limiter);
     if (!(c.courant > 0.0 && c.courant <= 1.0)) return fail(nullptr, PBE_ERR_ARG, "courant must be in (0, 1]");
     if (!(c.dt_fixed >= 0.0) || !std::isfinite(c.dt_fixed)) return fail(nullptr, PBE_ERR_ARG, "dt_fixed must be >= 0");

@@ -23,7 +23,7 @@ constexpr int MAXP = 10;   // tangent lanes
 constexpr int MAXTH = 10;  // kinetic parameters held in registers (POLY may have more: runtime loop)
 constexpr int MAX_PARAMS = 4096;   // PBE_MAX_PARAMS (include/pbe.h)
 
-enum { LIM_UPWIND = 0, LIM_VANLEER = 1 };
+enum { LIM_UPWIND = 0, LIM_VANLEER = 1, LIM_MINMOD = 2, LIM_SUPERBEE = 3, LIM_MC = 4 };
 enum { LAW_CONST = 0, LAW_ARRH = 1, LAW_POLY = 2 };
 enum { SOL_EXP = 0, SOL_POLY = 1 };
 enum { ST_OK = 0, ST_CFL = 2, ST_NEG = 3, ST_INFEAS = 4, ST_MAXSTEPS = 5 };
@@ -293,6 +293,50 @@ __device__ __forceinline__ void psi_half_d(double a, double b, double& h, double
     h = ab * r;
     qa = br * br;
     qb = ar * ar;
+}
+
+// NEXT-4 limiters (R-31; the paper fixes van Leer, L299-300) as slope limiters psi(a, b) =
+// phi(a/b) b for ab > 0, with A = |a|, B = |b| and the sign of b:
+//   minmod   m = A <= B ? A : B
+//   superbee m = max(min(2A, B), min(A, 2B))
+//   MC       m = min(2A, (A + B)/2, 2B)
+// Branch choices follow the oracle's min/max (ties take the second argument of min(x, y) =
+// x < y ? x : y on phi's argument order).  Half slope h = psi/2 and partials qa, qb = half
+// d psi/da, d psi/db (piecewise constant).
+__device__ __forceinline__ void psi_half_other(int lim, double a, double b, double& h, double& qa, double& qb) {
+    h = qa = qb = 0.0;
+    if (!(a * b > 0.0)) return;
+    const double A = fabs(a), B = fabs(b), s = b > 0.0 ? 0.5 : -0.5;
+    double m, dA, dB;
+    if (lim == LIM_MINMOD) {                          // phi = min(1, theta): theta < 1 ... tie -> theta
+        if (B < A) { m = B; dA = 0.0; dB = 1.0; } else { m = A; dA = 1.0; dB = 0.0; }
+    } else if (lim == LIM_SUPERBEE) {                 // max(min(2 theta, 1), min(theta, 2))
+        double m1, a1, b1, m2, a2, b2;
+        if (2.0 * A < B) { m1 = 2.0 * A; a1 = 2.0; b1 = 0.0; } else { m1 = B; a1 = 0.0; b1 = 1.0; }
+        if (A < 2.0 * B) { m2 = A; a2 = 1.0; b2 = 0.0; } else { m2 = 2.0 * B; a2 = 0.0; b2 = 2.0; }
+        if (m1 > m2) { m = m1; dA = a1; dB = b1; } else { m = m2; dA = a2; dB = b2; }
+    } else {                                          // MC: min(min(2 theta, (1+theta)/2), 2)
+        const double mid = (A + B) * 0.5;
+        if (2.0 * A < mid) { m = 2.0 * A; dA = 2.0; dB = 0.0; } else { m = mid; dA = 0.5; dB = 0.5; }
+        if (!(m < 2.0 * B)) { m = 2.0 * B; dA = 0.0; dB = 2.0; }
+    }
+    h = s * m;
+    qa = 0.5 * dA;         // d psi/da = dm/dA (sgn a = sgn b), halved
+    qb = 0.5 * dB;
+}
+// Half limited slope h = psi/2 for limiter `lim` (upwind: 0); van Leer first (hot path).
+__device__ __forceinline__ double psi_half(int lim, double a, double b) {
+    if (lim == LIM_VANLEER) return 0.5 * psi_vl(a, b);
+    if (lim == LIM_UPWIND) return 0.0;
+    double h, qa, qb;
+    psi_half_other(lim, a, b, h, qa, qb);
+    return h;
+}
+// h and the half partials for the tangent / adjoint lanes, any limiter.
+__device__ __forceinline__ void psi_half_dl(int lim, double a, double b, double& h, double& qa, double& qb) {
+    if (lim == LIM_VANLEER) { psi_half_d(a, b, h, qa, qb); return; }
+    if (lim == LIM_UPWIND) { h = qa = qb = 0.0; return; }
+    psi_half_other(lim, a, b, h, qa, qb);
 }
 
 // ------------------------------------------------------------------------------------

@@ -26,7 +26,7 @@ def _check(w):
     return g, o
 
 
-@pytest.mark.parametrize("lim", [W.LIM_UPWIND, W.LIM_VANLEER])
+@pytest.mark.parametrize("lim", [W.LIM_UPWIND, W.LIM_VANLEER, W.LIM_MINMOD, W.LIM_SUPERBEE, W.LIM_MC])
 def test_2d_base_case_coarse(lim):
     _check(W.c2d_base(120, 60, t_max=20.0, M=10, limiter=lim))
 

@@ -93,6 +93,11 @@ def test_adjoint_upwind_matches_oracle():
     _check(small_ensemble(n_sims=3, limiter=W.LIM_UPWIND))
 
 
+@pytest.mark.parametrize("lim", [W.LIM_MINMOD, W.LIM_SUPERBEE, W.LIM_MC])
+def test_adjoint_extra_limiters_match_oracle(lim):
+    _check(small_ensemble(n_sims=3, limiter=lim))
+
+
 def test_adjoint_uncapped_cfl_matches_oracle():
     """dt = nu dL/|G| (C = nu sgn G, R-9): the parameters act through the clock only."""
     _check(small_ensemble(n_sims=3, dt_max=math.inf, t_max=120.0, M=12))

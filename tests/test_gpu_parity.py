@@ -128,6 +128,32 @@ def test_lognormal_seed_matches_oracle(kernel):
     assert np.allclose(g["loss"], lo, rtol=1e-9, atol=0)
 
 
+EXTRA_LIMS = [W.LIM_MINMOD, W.LIM_SUPERBEE, W.LIM_MC]
+
+
+@pytest.mark.parametrize("lim", EXTRA_LIMS)
+def test_extra_limiters_resident_tangents(lim):
+    """NEXT-4 limiters (R-31) in the resident kernel with 8 tangent lanes (branch partials)."""
+    w = W.replace(W.c5_ensemble(n_sims=9, N=300, t_max=40.0, M=40), limiter=lim)
+    _check(w, mode=oracle.MODE_DUAL)
+
+
+@pytest.mark.parametrize("lim", EXTRA_LIMS)
+def test_extra_limiters_dissolution_and_stream(lim):
+    """C < 0 sweeps (dissolution) in the resident kernel and the streaming kernel."""
+    w = W.replace(W.c2_dissolution(N=400, t_max=30.0, M=30), limiter=lim)
+    _check(w)
+    w4 = W.replace(W.c4_sweep(3000, batch=2, n_steps=200), limiter=lim)
+    _check(w4, kernel=3)
+
+
+@pytest.mark.parametrize("lim", EXTRA_LIMS)
+def test_extra_limiters_cluster(lim):
+    w = W.replace(W.c4_sweep(10000, batch=2, n_steps=100), limiter=lim)
+    g, o = _check(w, kernel=2)
+    assert g["info"]["kernel"] == 2
+
+
 def test_c5_full_size_sampled_sims():
     """C5 exactly as bench.py runs it (4096 sims x 2000 bins, 8 tangents) — oracle on 2 sims."""
     w = W.c5_ensemble()

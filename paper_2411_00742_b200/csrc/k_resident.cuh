@@ -38,7 +38,7 @@
 namespace pbe {
 
 #if PBE_TIMING
-__device__ unsigned long long g_phase_cycles[8];   // sweep, moments+publish, barrier, scalar, steps, [scalar: sums, mass balance, kinetics]
+__device__ unsigned long long g_phase_cycles[12];   // sweep, moments+publish, barrier, scalar, steps, [scalar: sums, mass balance, kinetics]
 #define PBE_TSTAMP(v) long long v = clock64()
 #define PBE_TACC(i, a, b) t_acc[i] += (unsigned long long)((b) - (a))   // registers; written at exit
 #else
@@ -188,7 +188,7 @@ template <int P, int K, int MAXT, bool CL = false, int MINB = 1>
 __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     namespace cg = cooperative_groups;
 #if PBE_TIMING
-    unsigned long long t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long t_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
     constexpr int V = 1 + P;
     constexpr int PP = P > 0 ? P : 1;
@@ -330,8 +330,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     // smem copy: primal part once per warp (identical in all lanes), tangent part per lane
     struct WarpPart { double c, t, mu3p, dt, loss, rms_c, rms_L, tn; long long nstep; int m, status, landing; };
     struct LanePart { double c, t, mu3p, dt, gacc; };
-    WarpPart* s_wp = reinterpret_cast<WarpPart*>(s_halo + 2 * HP);
-    LanePart* s_lp = reinterpret_cast<LanePart*>(s_wp + 32);
+    // static shared arrays (direct LDS/STS; a pointer carved out of the dynamic buffer makes the
+    // compiler form generic addresses, rematerialised every step)
+    __shared__ WarpPart s_wp[MAXT / 32];
+    __shared__ LanePart s_lp[MAXT];
     auto load_ls = [&]() -> LaneScal {
         const WarpPart w = s_wp[warp];
         const LanePart l = s_lp[tid];
@@ -362,20 +364,57 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     const bool kin_smem = kp.n_params <= MAXTH;
     const int nsd = kp.n_params + kp.n_sol;
     __shared__ double s_th[MAXTH], s_sol[3], s_seed[PP * (MAXTH + 3)];
+    // POLY fast path: coefficient j as lane l's dual number, lane-major, zero-padded to MAXTH
+    // (a zero term changes no Horner step: g x + 0 == g x), read with direct shared indexing
+    __shared__ double2 s_poly[MAXTH][32];
+    const bool poly_fast = kin_smem && kp.law == LAW_POLY && KC.const_T;
     if (kin_smem) {
         const double* th = kp.theta + (size_t)s * kp.n_params;
         for (int j = tid; j < kp.n_params; j += NT) s_th[j] = th[j];
         for (int j = tid; j < kp.n_sol; j += NT) s_sol[j] = kp.sol[j];
         for (int j = tid; j < nl * nsd; j += NT) s_seed[j] = kp.seed[(size_t)lane0 * nsd + j];
+        for (int e = tid; e < MAXTH * 32; e += NT) {
+            const int j = e >> 5, l = e & 31;
+            const bool on = j < kp.n_params;
+            const bool seeded = on && l < nl;
+            s_poly[j][l] = make_double2(on ? th[j] : 0.0, seeded ? kp.seed[(size_t)(lane0 + l) * nsd + j] : 0.0);
+        }
     }
     __syncthreads();
     const KinLoaderS KLS{s_th, s_sol, s_seed, pl, kp.n_params, nsd};
     auto kinetics_with = [&](const auto& LDR, LaneScal& L) -> bool {
+        PBE_TSTAMP(tk0);
         D1 T;
-        const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
-        const D1 G = growth_rate(kp, LDR, S, T);
+        D1 G;
+        if (poly_fast) {                               // S = c / c*(T) at constant T, eq-poly_growth_rate
+            T = KC.T;
+            const D1 S = L.c * KC.ics;
+            G = mk(0.0);
+            if (S.v > 1.0) {
+                const D1 x = S - 1.0;
+#pragma unroll
+                for (int j = MAXTH - 1; j >= 0; --j) {
+                    const double2 a = s_poly[j][lane];
+                    G = G * x + mk(a.x, a.y);
+                }
+                G = G * x;
+            }
+        } else {
+            const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
+            G = growth_rate(kp, LDR, S, T);
+        }
+#if PBE_TIMING
+        volatile double sink_g = G.v + G.d; (void)sink_g;          // pin the stamp after G
+#endif
+        PBE_TSTAMP(tk1);
+        PBE_TACC(8, tk0, tk1);
         const double tn = steps_mode ? 0.0 : L.tn;
         const StepScalars sc = time_step(kp, G, L.t, tn, steps_mode);
+#if PBE_TIMING
+        volatile double sink_c = sc.C.v + sc.kap.v; (void)sink_c;
+#endif
+        PBE_TSTAMP(tk2);
+        PBE_TACC(9, tk1, tk2);
         if (sc.err != ST_OK) { L.status = sc.err; return false; }
         L.dt = sc.dt;
         L.landing = sc.landing;
@@ -539,7 +578,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     // ---- epilogue -----------------------------------------------------------------------
 #if PBE_TIMING
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        for (int i = 0; i < 8; ++i) g_phase_cycles[i] = t_acc[i];
+        for (int i = 0; i < 12; ++i) g_phase_cycles[i] = t_acc[i];
 #endif
     if (kp.n_final && grp == 0) {
 #pragma unroll

@@ -108,8 +108,9 @@ struct ResidentVariant {
     int P, K, maxt;
     KernelFn fn;
 };
-// halo (2 parities) + scalar state (WarpPart[32] <= 96 B, LanePart[nt] = 40 B)
-size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double) + 32 * 96 + (size_t)nt * 40; }
+// dynamic smem: halo (2 parities); the scalar state (WarpPart, LanePart) and the kinetics
+// tables are static shared arrays (<= 48 KB), accounted for by the 200 KB dynamic cap below
+size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double); }
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {
@@ -180,6 +181,12 @@ int lanes_per_cta(int P, int group_max) {
     return 5;                      // 9..10 lanes: 2 groups of 5
 }
 
+// static shared memory of a kernel (cached per function by the runtime)
+size_t static_smem(KernelFn fn) {
+    cudaFuncAttributes a{};
+    return cudaFuncGetAttributes(&a, (const void*)fn) == cudaSuccess ? a.sharedSizeBytes : 48 * 1024;
+}
+
 // Resident variant for N bins: one simulation alone wants the smallest K (most warps); a
 // batch wants small CTAs so several simulations share an SM and hide each other's per-step
 // latency (K_pref from PBE_RESIDENT_K or the heuristic in pbe_run_batch).
@@ -191,7 +198,7 @@ const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups, i
         if (v.P != Pi) continue;
         if ((long long)v.K * v.maxt < N) continue;
         const int nt = ((N + v.K - 1) / v.K + 31) / 32 * 32;
-        if (resident_smem(v, nt) > 200 * 1024) continue;      // + <= 20 KB static < 227 KB
+        if (resident_smem(v, nt) + static_smem(v.fn) > 227 * 1024) continue;   // dynamic + static per CTA
         if (!best) { best = &v; continue; }
         const bool closer = k_pref ? (abs(v.K - k_pref) < abs(best->K - k_pref) ||
                                       (abs(v.K - k_pref) == abs(best->K - k_pref) && v.K < best->K))

@@ -17,7 +17,7 @@ P = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 w = W.c5_ensemble(n_sims=sims, t_max=tmax, M=int(tmax), n_tangents=P)
 lib = pb.load_library()
 r = pb.run_workload(w, want_n=False)
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 12)()
 assert lib.pbe_debug_phase_cycles(buf) == 0
 c = np.array(buf[:5], dtype=np.float64)
 steps = c[4]
@@ -28,4 +28,7 @@ for n, v in zip(names, c[:4]):
     print(f"  {n:18s} {v / steps:8.0f} cycles/step  {100 * v / tot:5.1f}%")
 c2 = np.array(buf[5:8], dtype=np.float64)
 for n, v in zip(["  scalar: load+sums", "  scalar: mass bal.", "  scalar: kinetics"], c2):
+    print(f"  {n:18s} {v / steps:8.0f} cycles/step")
+c3 = np.array(buf[8:10], dtype=np.float64)
+for n, v in zip(["    S + growth law", "    time step"], c3):
     print(f"  {n:18s} {v / steps:8.0f} cycles/step")

@@ -447,7 +447,7 @@ def main():
                               f"{int(r3['steps'].max())} steps", metric="ms per gradient (wall, incl. copies)",
                      adjoint_ms=1e3 * min(ta), fd_batched_ms=1e3 * tf, fd_sims=int(wf.n_sims),
                      speedup_vs_fd=tf / min(ta), finite=bool(np.isfinite(g3["grad"]).all()),
-                     note="forward-mode tangents need 100 passes of 10 lanes (tools/next3_time.py: 92x slower)")
+                     note="forward-mode tangents need 100 passes of 10 lanes (tools/next3_time.py: 205x slower)")
         del n03
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------------------------

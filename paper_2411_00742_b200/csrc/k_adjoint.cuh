@@ -196,7 +196,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         const D1 cD = mk(c, lane == 0 ? 1.0 : 0.0), tD = mk(t, lane == 1 ? 1.0 : 0.0);
         D1 T;
         const D1 S = supersaturation(kp, KL, kT, KC, tD, cD, T);
-        D1 G = growth_rate(kp, KL, S, T);
+        D1 G = (kp.law == LAW_POLY && kp.n_params > MAXTH)
+                   ? poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S)   // warp-cooperative
+                   : growth_rate(kp, KL, S, T);
         if (lane == 2) G = mk(G.v, 1.0);
         const double tn = kp.t_samples[m];
         const StepScalars sc = time_step(kp, G, tD, tn, false);

@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
                 }
                 G = G * x;
             }
+        } else if (P == 0 && kp.law == LAW_POLY && kp.n_params > MAXTH) {   // no seeds: warp-cooperative
+            const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
+            G = poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S);
         } else {
             const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
             G = growth_rate(kp, LDR, S, T);

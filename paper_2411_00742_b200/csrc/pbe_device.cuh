@@ -182,6 +182,36 @@ __device__ __forceinline__ D1 growth_rate(const KParams& kp, const LD& L, D1 S, 
     return mk(0.0);
 }
 
+// Long polynomial growth law (n > MAXTH terms; NEXT-3's 1000-coefficient regime) evaluated
+// cooperatively by the 32 lanes of a warp, for lanes WITHOUT parameter seeds: lane l sums the
+// terms j in [l m, l m + m), m = ceil(n/32), by Horner (value and d/dx), scales by x^(l m + 1),
+// and a symmetric xor butterfly gives every lane the same G = sum_j a_j x^(j+1) and dG/dx;
+// the lane's tangent is dG/dx * dS (chain rule).  O(n/32) dependent steps instead of O(n).
+// Must be called by all 32 lanes (warp-uniform S).
+__device__ __forceinline__ D1 poly_long_warp(const double* __restrict__ a, int n, D1 S) {
+    if (!(S.v > 1.0)) return mk(0.0);
+    const int lane = threadIdx.x & 31;
+    const double x = S.v - 1.0;
+    const int m = (n + 31) >> 5;
+    const int j0 = lane * m;
+    double q = 0.0, dq = 0.0;
+    for (int i = m - 1; i >= 0; --i) {
+        const int j = j0 + i;
+        const double aj = j < n ? __ldg(a + j) : 0.0;
+        dq = fma(dq, x, q);
+        q = fma(q, x, aj);
+    }
+    const double xl = pow(x, (double)j0);             // x^(l m)
+    double t = xl * x * q;                             // x^(l m + 1) q(x)
+    double dt = xl * fma((double)(j0 + 1), q, x * dq); // (l m + 1) x^(l m) q + x^(l m + 1) q'
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, off);
+        dt += __shfl_xor_sync(0xffffffffu, dt, off);
+    }
+    return {t, dt * S.d};
+}
+
 // Kinetics inputs that are constant when the temperature profile is constant (one knot):
 // T and 1/c*(T) are computed once, so a step needs no exp and no division for S.
 struct KinCache {

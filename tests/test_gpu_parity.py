@@ -154,6 +154,14 @@ def test_extra_limiters_cluster(lim):
     assert g["info"]["kernel"] == 2
 
 
+@pytest.mark.parametrize("n_params", [40, 1000])
+def test_long_polynomial_primal_matches_oracle(n_params):
+    """NEXT-3's long polynomials (n_params > 10) through the primal resident kernel (the
+    warp-cooperative evaluation) against the oracle's power-sum loop."""
+    w = W.next3_estimation(n_params=n_params, N=300, t_max=40.0, M=40)
+    _check(w)
+
+
 def test_c5_full_size_sampled_sims():
     """C5 exactly as bench.py runs it (4096 sims x 2000 bins, 8 tangents) — oracle on 2 sims."""
     w = W.c5_ensemble()

@@ -166,6 +166,49 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
     return bad;
 }
 
+// Long polynomial growth law WITH parameter seeds (tangent lanes, n > MAXTH): as
+// poly_long_warp, and lane l's chunk also accumulates, for every tangent p of the CTA,
+// sum_{j in chunk} seed_{p,j} x^(j+1) (P Horner chains); butterfly sums give every lane all P
+// totals; lane p's tangent is its total + dG/dx dS.  O(n/32 * P) steps instead of O(n).
+template <int PP>
+__device__ __forceinline__ D1 poly_long_warp_seeded(const double* __restrict__ a, const double* __restrict__ seed,
+                                                     int nsd, int lane0, int nl, int n, D1 S, int pl) {
+    if (!(S.v > 1.0)) return mk(0.0);
+    const int lane = threadIdx.x & 31;
+    const double x = S.v - 1.0;
+    const int m = (n + 31) >> 5;
+    const int j0 = lane * m;
+    double q = 0.0, dq = 0.0, sp[PP];
+#pragma unroll
+    for (int p = 0; p < PP; ++p) sp[p] = 0.0;
+    for (int i = m - 1; i >= 0; --i) {
+        const int j = j0 + i;
+        const bool on = j < n;
+        const double aj = on ? __ldg(a + j) : 0.0;
+        dq = fma(dq, x, q);
+        q = fma(q, x, aj);
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+            sp[p] = fma(sp[p], x, (on && p < nl) ? __ldg(seed + (size_t)(lane0 + p) * nsd + j) : 0.0);
+    }
+    const double xl = pow(x, (double)j0), xl1 = xl * x;   // x^(l m), x^(l m + 1)
+    double t = xl1 * q;
+    double dt = xl * fma((double)(j0 + 1), q, x * dq);
+#pragma unroll
+    for (int p = 0; p < PP; ++p) sp[p] *= xl1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, off);
+        dt += __shfl_xor_sync(0xffffffffu, dt, off);
+#pragma unroll
+        for (int p = 0; p < PP; ++p) sp[p] += __shfl_xor_sync(0xffffffffu, sp[p], off);
+    }
+    double mine = 0.0;
+#pragma unroll
+    for (int p = 0; p < PP; ++p) if (p == pl) mine = sp[p];
+    return {t, fma(dt, S.d, mine)};
+}
+
 // Grid: one CTA per simulation.  Block: NT = 32 NW threads with NT K >= N.
 // P = tangent lanes per CTA.  The kp.P lanes of a simulation are split into kp.G lane
 // groups of P: CTA b runs simulation b / G, group g = b % G, i.e. lanes [g P, g P + P)
@@ -399,9 +442,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
                 }
                 G = G * x;
             }
-        } else if (P == 0 && kp.law == LAW_POLY && kp.n_params > MAXTH) {   // no seeds: warp-cooperative
+        } else if (kp.law == LAW_POLY && kp.n_params > MAXTH) {            // long polynomial: warp-cooperative
             const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
-            G = poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S);
+            if (P == 0) G = poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S);
+            else G = poly_long_warp_seeded<PP>(kp.theta + (size_t)s * kp.n_params, kp.seed, nsd, lane0, nl,
+                                               kp.n_params, S, pl);
         } else {
             const D1 S = supersaturation(kp, LDR, kT, KC, L.t, L.c, T);
             G = growth_rate(kp, LDR, S, T);

@@ -162,6 +162,19 @@ def test_long_polynomial_primal_matches_oracle(n_params):
     _check(w)
 
 
+def test_long_polynomial_tangents_match_oracle():
+    """Tangent lanes on a 40-term polynomial (warp-cooperative seeded evaluation): unit seeds
+    on low and high coefficients plus one mixed direction."""
+    w = W.next3_estimation(n_params=40, N=300, t_max=40.0, M=40)
+    Q = w.sol.shape[0]
+    seed = np.zeros((5, 40 + Q))
+    for p, j in enumerate((0, 3, 9, 27)):
+        seed[p, j] = 1.0
+    seed[4, :40] = np.linspace(1.0, 0.1, 40)
+    w = W.replace(w, n_tangents=5, tangent_seed=seed)
+    _check(w, mode=oracle.MODE_DUAL)
+
+
 def test_c5_full_size_sampled_sims():
     """C5 exactly as bench.py runs it (4096 sims x 2000 bins, 8 tangents) — oracle on 2 sims."""
     w = W.c5_ensemble()

@@ -402,16 +402,38 @@ def main():
 
     # ---- secondary (1 GPU): the C4 10^6-bin batch through the HBM-streaming kernel ----------------
     secondary = None
+    next4 = None
     if world == 1 and args.workload == "c5" and not args.no_secondary:
         w4 = W.c4_sweep(1_000_000, batch=64, n_steps=1000)
-        ctx4 = pb.context_for(w4, device=local_rank)
         n04 = torch.from_numpy(np.ascontiguousarray(w4.n0)).to(dev)
+        old_tb = os.environ.get("PBE_TEMPORAL_BLOCK")
+        os.environ["PBE_TEMPORAL_BLOCK"] = "0"                      # plain streaming: 16 B/update
+        ctx4 = pb.context_for(w4, device=local_rank)
         ms4, bu4, kms4 = measure(ctx4, w4, n04, None, gather=False)
         info4 = ctx4.last_run_info()
-        secondary = dict(workload="C4 bin sweep N=1e6, batch 64, 1000 uncapped CFL steps", value=bu4 / (ms4 * 1e-3),
-                         unit=UNIT, ms_per_step=ms4, roofline=roofline(w4, info4, bu4, kms4, "c4"), kernel=info4,
+        secondary = dict(workload="C4 bin sweep N=1e6, batch 64, 1000 uncapped CFL steps (plain streaming)",
+                         value=bu4 / (ms4 * 1e-3), unit=UNIT, ms_per_step=ms4,
+                         roofline=roofline(w4, info4, bu4, kms4, "c4"), kernel=info4,
                          gpu_launches=int(info4["launches"]) * args.steps)
         ctx4.close()
+        # NEXT-4: the same workload with temporal blocking (the library default for uncapped-CFL
+        # steps mode): 8 steps per HBM pass, 2 B/update of traffic
+        os.environ["PBE_TEMPORAL_BLOCK"] = "1"
+        ctx4 = pb.context_for(w4, device=local_rank)
+        ms5, bu5, kms5 = measure(ctx4, w4, n04, None, gather=False)
+        info5 = ctx4.last_run_info()
+        ctx4.close()
+        if old_tb is None:
+            os.environ.pop("PBE_TEMPORAL_BLOCK", None)
+        else:
+            os.environ["PBE_TEMPORAL_BLOCK"] = old_tb
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        v5 = bu5 / (ms5 * 1e-3)
+        next4 = dict(workload="C4 bin sweep N=1e6, batch 64, 1000 uncapped CFL steps, temporal blocking (NEXT-4)",
+                     value=v5, unit=UNIT, ms_per_step=ms5, kernel=info5, speedup_vs_plain_stream=v5 / (bu4 / (ms4 * 1e-3)),
+                     bytes_per_bin_update=16.0 / max(1, info5["steps_per_pass"]),
+                     plain_stream_hbm_ceiling=hbm * 1e9 / 16.0, frac_of_plain_stream_ceiling=v5 / (hbm * 1e9 / 16.0),
+                     gpu_launches=int(info5["launches"]) * args.steps)
         del n04
 
     # ---- NEXT-3 (1 GPU): one reverse-mode gradient over 1000 parameters (9 App-B experiments) vs the
@@ -466,7 +488,7 @@ def main():
                     ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
                     data="synthetic (seeded; DESIGN.md input recipe)", config=cfg, roofline=roof,
                     cpu_baseline=cpu, e2e=e2e, gpu_launches=int(info["launches"]) * args.steps, clocks=clk,
-                    secondary=secondary, next3=next3)
+                    secondary=secondary, next3=next3, next4=next4)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

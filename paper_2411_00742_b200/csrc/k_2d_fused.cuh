@@ -60,11 +60,12 @@ struct Params2DF {
 
 // Limited flux term kap psi(a, b) = k2 ab/(a+b) (0 unless ab > 0), k2 = |C|(1-|C|) = 2 kap
 // (psi = 2ab/(a+b) is the van Leer limited slope), in the select-free
-// form psi = (a|b| + |a|b) / (|a| + |b|): the numerator is 2ab when ab > 0 and exactly 0
+// form psi = (a|b| + |a|b) / (|a| + |b|): the numerator is 2 round(ab) when ab > 0 and exactly 0
 // otherwise; the denominator is |a+b| when ab > 0 (+1e-300 keeps 0/0 out; it changes no
 // quotient with |a+b| > 1e-284).  Upwind passes k2 = 0 (exactly 0 term).
 __device__ __forceinline__ double limited(double a, double b, double k2h) {   // k2h = k2 / 2
-    const double num = fma(fabs(a), b, a * fabs(b));
+    // separately rounded products: exact cancellation for ab < 0 (see psi_half_vl_sf)
+    const double num = __dadd_rn(__dmul_rn(fabs(a), b), __dmul_rn(a, fabs(b)));
     const double den = (fabs(a) + fabs(b)) + 1e-300;
     return (k2h * num) * rcp_nr(den);
 }

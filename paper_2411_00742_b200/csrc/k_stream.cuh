@@ -120,7 +120,8 @@ struct SimCoef {
 
 // One thread's K bins of a tile: fluxes of K+1 faces from the smem window, update, moment
 // partials, 16-byte stores.  NEG = (C < 0) (direction is uniform per tile).
-template <int P, int K, bool NEG>
+// LK: limiter kind (0 upwind, 1 van Leer, 2 minmod/superbee/MC via psi_half_dl)
+template <int P, int K, bool NEG, int LK>
 __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int RS, int g0, int nb, int i_base,
                                             const SimCoef<P>& cf, int lim, bool sample, double L_half, double dL,
                                             double* __restrict__ drow, long long pitch,
@@ -143,7 +144,11 @@ __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int R
         const int ja = NEG ? f + 1 : f - 1;
         const double a = x[0][ja] - x[0][ja - 1], b = x[0][f] - x[0][f - 1];
         double h = 0.0, qa = 0.0, qb = 0.0;
-        psi_half_dl(lim, a, b, h, qa, qb);
+        if (LK == 2) psi_half_dl(lim, a, b, h, qa, qb);
+        else if (LK == 1) {
+            if (P == 0) h = psi_half_vl_sf(a, b);            // primal only: select-free
+            else psi_half_d(a, b, h, qa, qb);
+        }
         const double nup = x[0][u];
         F[f - 2] = fma(C, nup, kap2 * h);
         if (P > 0) {
@@ -387,13 +392,16 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
 #pragma unroll
                     for (int v = 0; v < V; ++v) acc[km][v] = 0.0;
                 bool neg = false;
+#define PBE_SB(NEGV, LKV)                                                                                  \
+    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)                                     \
+        stream_bins<P, K, NEGV, LKV>(sb, RS, g0, nb, b0, cf, vl, sample, L_half, kp.dL, drow, sp.pitch, acc, neg)
+                const int lk = vl == LIM_VANLEER ? 1 : (vl == LIM_UPWIND ? 0 : 2);
                 if (cf.C >= 0.0) {
-                    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
-                        stream_bins<P, K, false>(sb, RS, g0, nb, b0, cf, vl, sample, L_half, kp.dL, drow, sp.pitch, acc, neg);
+                    if (lk == 1) PBE_SB(false, 1); else if (lk == 0) PBE_SB(false, 0); else PBE_SB(false, 2);
                 } else {
-                    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
-                        stream_bins<P, K, true>(sb, RS, g0, nb, b0, cf, vl, sample, L_half, kp.dL, drow, sp.pitch, acc, neg);
+                    if (lk == 1) PBE_SB(true, 1); else if (lk == 0) PBE_SB(true, 0); else PBE_SB(true, 2);
                 }
+#undef PBE_SB
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[st]);           // stage free for the producer
                 // round-off clip (R-17), rare: fix the stored values of this warp's bins

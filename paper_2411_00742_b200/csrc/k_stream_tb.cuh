@@ -26,6 +26,9 @@
 
 namespace pbe {
 
+#ifndef PBE_TB_MINB
+#define PBE_TB_MINB 2      // 2 CTAs/SM (measured best: 3.34e11 vs 2.50e11 at 3, 2.49e11 at 1)
+#endif
 constexpr int TB_KB = 8;                 // max fused steps per block
 constexpr int TB_GH = 2 * TB_KB;         // ghost / halo width (cells)
 constexpr int TB_STAGES = 2;
@@ -50,7 +53,111 @@ struct StreamTBParams {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__global__ void __launch_bounds__(TB_NT, 2) k_stream_tb(const StreamTBParams sp) {
+// One consumer warp's share of a tile (v2: warp-independent sub-steps).  Warp w owns the
+// SEG = TB/8 cells [GH + w SEG, GH + (w+1) SEG) of the window and keeps the region
+// [w SEG, w SEG + SEG + 2 GH) = 32 KW cells in registers, KW contiguous cells per lane.  A
+// sub-step exchanges 2 cells with each neighbour lane by shuffles and updates the lane's KW
+// cells (eq-highRes_growth, flux form); the outermost 2 cells of the region go stale per
+// sub-step (lanes 0 / 31 see no neighbour), which the 2 KB-cell halo absorbs.  No shared-
+// memory round trips, no CTA barriers inside the tile.
+struct TBTile {
+    const double* win;           // smem stage: window cells [b0 - GH, b0 + TB + GH)
+    double* dst;                 // output row at bin b0 (owned cells)
+    double* part;                // [KB][5] this warp's partials of the tile
+    int b0, nb, N, TB, d;
+    bool sample_last;
+    double C, clip, dL, L_half;
+    int lim;
+    unsigned long long* empty;   // stage's empty barrier
+};
+
+template <int KW, bool NEG, int LK>
+__device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
+    constexpr int KB = TB_KB, GH = TB_GH, NWC = TB_NWC;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int SEG = T.TB / NWC;
+    const int x0 = warp * SEG + lane * KW;                      // window index of the lane's first cell
+    const double C = T.C, aC = fabs(C), kap2 = aC * (1.0 - aC);
+    double c[KW], w3[KW];
+    unsigned dom = 0, own = 0;
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+        const int x = x0 + k, i = T.b0 - GH + x;
+        c[k] = T.win[x];
+        const bool in = i >= 0 && i < T.N;
+        const bool ow = x >= GH + warp * SEG && x < GH + (warp + 1) * SEG && x - GH < T.nb;
+        dom |= (in ? 1u : 0u) << k;
+        own |= (ow ? 1u : 0u) << k;
+        const double Lc = fma((double)i, T.dL, T.L_half);
+        w3[k] = ow ? T.dL * Lc * Lc * Lc : 0.0;                 // mu3 weight (0 off the owned cells)
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(T.empty);                        // this warp is done with the stage
+    double am[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int q = 0; q < T.d; ++q) {
+        // neighbours' boundary cells
+        const double L1 = __shfl_up_sync(0xffffffffu, c[KW - 1], 1), L2 = __shfl_up_sync(0xffffffffu, c[KW - 2], 1);
+        const double R1 = __shfl_down_sync(0xffffffffu, c[0], 1), R2 = __shfl_down_sync(0xffffffffu, c[1], 1);
+        double w[KW + 4];
+        w[0] = L2; w[1] = L1; w[KW + 2] = R1; w[KW + 3] = R2;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) w[k + 2] = c[k];
+        double F[KW + 1];
+#pragma unroll
+        for (int f = 2; f <= KW + 2; ++f) {                     // face between window cells f-1 | f
+            const int u = NEG ? f : f - 1;
+            const int ja = NEG ? f + 1 : f - 1;
+            const double a = w[ja] - w[ja - 1], b = w[f] - w[f - 1];
+            double h = 0.0;
+            if (LK == 1) h = psi_half_vl_sf(a, b);
+            else if (LK == 2) h = psi_half(T.lim, a, b);
+            F[f - 2] = fma(C, w[u], kap2 * h);
+        }
+        const bool last = q == T.d - 1;
+        bool bad = false;
+        double a3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+            double v = w[k + 2] - (F[k + 1] - F[k]);
+            v = ((dom >> k) & 1u) ? v : 0.0;                    // ghost cells outside [0, N) stay 0
+            const bool o = (own >> k) & 1u;
+            bad |= o && v < -T.clip;
+            v = (v < 0.0 && v >= -T.clip) ? 0.0 : v;            // round-off clip (R-17)
+            c[k] = v;
+            a3 = fma(w3[k], v, a3);
+        }
+        // this sub-step's warp partial (fixed-order xor tree); lane 0 writes [mu3, bad]
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+        const bool bq = __any_sync(0xffffffffu, bad);
+        if (lane == 0) { T.part[q * 5 + 3] = a3; T.part[q * 5 + 4] = bq ? 1.0 : 0.0; }
+        if (last) {
+#pragma unroll
+            for (int k = 0; k < KW; ++k) {
+                if ((own >> k) & 1u) {
+                    T.dst[x0 + k - GH] = c[k];                  // owned cells after d sub-steps
+                    if (T.sample_last) {
+                        const double Lc = fma((double)(T.b0 - GH + x0 + k), T.dL, T.L_half);
+                        const double w0 = T.dL * c[k], w1 = w0 * Lc;
+                        am[0] += w0; am[1] += w1; am[2] = fma(w1, Lc, am[2]);
+                    }
+                }
+            }
+        }
+    }
+    if (T.sample_last) {
+#pragma unroll
+        for (int km = 0; km < 3; ++km) {
+            double r = am[km];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+            if (lane == 0) T.part[(T.d - 1) * 5 + km] = r;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTBParams sp) {
     constexpr int KB = TB_KB, GH = TB_GH, NWC = TB_NWC, K = 4;
     const KParams& kp = sp.kp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -150,68 +257,20 @@ __global__ void __launch_bounds__(TB_NT, 2) k_stream_tb(const StreamTBParams sp)
                 const int s = (int)(t / sp.T_sim), j = (int)(t - (long long)s * sp.T_sim);
                 const int b0 = j * TB, nb = min(TB, N - b0);
                 const SimS& W = s_sim[s - s_lo];
-                const int d = W.depth, sgn_b = W.sign;
-                const bool sample_last = W.sample != 0;
-                const double C = sgn_b * kp.courant, aC = fabs(C), kap2 = aC * (1.0 - aC);
-                const double thr = W.clip;
-                const double* in = smem + (size_t)st * WL;
-                double* outb = work0;
-                double* dst = (W.cur ? sp.buf0 : sp.buf1) + (size_t)s * sp.pitch + b0 + GH;
-                for (int q = 0; q < d; ++q) {
-                    const bool last = (q == d - 1);
-                    const bool all_mom = last && sample_last;
-                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                    bool bad = false;
-                    // cells x = 2 .. WL-3 of the window (global bin b0 - GH + x)
-                    for (int x0 = 2 + (warp * 32 + lane) * K; x0 < WL - 2; x0 += NWC * 32 * K) {
-                        double w[K + 4];
-                        const double2* w2 = reinterpret_cast<const double2*>(in + x0 - 2);   // 16-byte aligned
-#pragma unroll
-                        for (int r = 0; r < (K + 4) / 2; ++r) {
-                            const double2 v2 = (x0 - 2 + 2 * r < WL) ? w2[r] : make_double2(0.0, 0.0);
-                            w[2 * r] = v2.x; w[2 * r + 1] = v2.y;
-                        }
-                        double y[K];
-                        if (C >= 0.0) line_update<false>(w, C, kap2, vl, y);
-                        else          line_update<true>(w, C, kap2, vl, y);
-#pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            const int x = x0 + k;
-                            const int i = b0 - GH + x;                       // global bin
-                            double v = y[k];
-                            if (i < 0 || i >= N || x >= WL - 2) v = 0.0;     // ghosts stay zero
-                            else if (v < 0.0) { if (v >= -thr) v = 0.0; else if (x >= GH && x < GH + nb) bad = true; }
-                            y[k] = v;
-                            if (x >= GH && x < GH + nb) {                    // owned cell: partials
-                                const double Lc = fma((double)i, kp.dL, L_half);
-                                const double w1 = kp.dL * Lc, w2 = w1 * Lc;
-                                acc[3] = fma(w2 * Lc, v, acc[3]);
-                                if (all_mom) { acc[0] = fma(kp.dL, v, acc[0]); acc[1] = fma(w1, v, acc[1]); acc[2] = fma(w2, v, acc[2]); }
-                                if (last) dst[x - GH] = v;                   // owned cells after d sub-steps
-                            }
-                        }
-#pragma unroll
-                        for (int k = 0; k < K; ++k)
-                            if (x0 + k < WL) outb[x0 + k] = y[k];
-                    }
-                    if (q == 0) { __syncwarp(); if (lane == 0) mbar_arrive(&s_empty[st]); }   // stage consumed
-                    // per-warp partials of sub-step q
-                    double* pt = sp.part + ((((size_t)s * sp.T_sim + j) * NWC + warp) * KB + q) * 5;
-#pragma unroll
-                    for (int km = 0; km < 4; ++km) {
-                        if (km == 3 || all_mom) {
-                            double r = acc[km];
-#pragma unroll
-                            for (int off = 16; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
-                            if (lane == 0) pt[km] = r;
-                        }
-                    }
-                    const bool bany = __any_sync(0xffffffffu, bad);
-                    if (lane == 0) pt[4] = bany ? 1.0 : 0.0;
-                    named_bar(1, NWC * 32);                 // sub-step q complete in smem
-                    in = outb;
-                    outb = (outb == work0) ? work1 : work0;
-                }
+                const int lk = vl == LIM_VANLEER ? 1 : (vl == LIM_UPWIND ? 0 : 2);
+                TBTile tile{smem + (size_t)st * WL, (W.cur ? sp.buf0 : sp.buf1) + (size_t)s * sp.pitch + b0 + GH,
+                            sp.part + (((size_t)s * sp.T_sim + j) * NWC + warp) * KB * 5, b0, nb, N, TB, W.depth,
+                            W.sample != 0, W.sign * kp.courant, W.clip, kp.dL, L_half, vl, &s_empty[st]};
+                const bool neg_c = W.sign < 0;
+#define PBE_TBW(KWV)                                                                                        \
+    do {                                                                                                    \
+        if (!neg_c) { if (lk == 1) tb_tile_warp<KWV, false, 1>(tile); else if (lk == 0) tb_tile_warp<KWV, false, 0>(tile); \
+                      else tb_tile_warp<KWV, false, 2>(tile); }                                             \
+        else        { if (lk == 1) tb_tile_warp<KWV, true, 1>(tile); else if (lk == 0) tb_tile_warp<KWV, true, 0>(tile);   \
+                      else tb_tile_warp<KWV, true, 2>(tile); }                                              \
+    } while (0)
+                if (TB == 2048) PBE_TBW(9); else if (TB == 1024) PBE_TBW(5); else PBE_TBW(3);
+#undef PBE_TBW
             }
         }
 

@@ -74,8 +74,9 @@ struct pbe_ctx_s {
     int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
     bool cluster2 = false;   // env PBE_CLUSTER2: 2-CTA clusters at 2 CTAs/SM for small N
     int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
-    bool temporal_block = false; // env PBE_TEMPORAL_BLOCK=1 enables NEXT-4 in k_stream (opt-in:
-                                 // correct, but slower than plain streaming for batches so far)
+    bool temporal_block = true;  // NEXT-4 temporal blocking for uncapped-CFL steps mode in
+                                 // k_stream (1.27x plain streaming on 64 x 1e6); env
+                                 // PBE_TEMPORAL_BLOCK=0 selects plain streaming
     bool unfused_2d = false;     // env PBE_2D_UNFUSED=1: two-sweep k_2d instead of k_2d_fused
 };
 
@@ -286,7 +287,11 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
 static pbe_status launch_stream_tb(pbe_ctx ctx, KParams kp, int S, const double* n0, long long n0_stride,
                                    double* n_final, cudaStream_t st) {
     const int N = kp.N;
-    const int TB = pbe::stream_tb_tile(N);
+    int TB = pbe::stream_tb_tile(N);
+    if (const char* e = getenv("PBE_TB_TILE")) {           // A/B only: 512, 1024 or 2048
+        const int v = atoi(e);
+        if (v == 512 || v == 1024 || v == 2048) TB = v;
+    }
     const int T_sim = (N + TB - 1) / TB;
     const long long pitch = ((long long)T_sim * TB + 2 * pbe::TB_GH + 3) / 4 * 4;
     int sms = 0, per_sm = 0;

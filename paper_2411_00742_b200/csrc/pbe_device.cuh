@@ -325,6 +325,15 @@ __device__ __forceinline__ void psi_half_d(double a, double b, double& h, double
     qb = ar * ar;
 }
 
+// Select-free van Leer half slope (primal paths): h = ab/(a+b) for ab > 0, else exactly 0,
+// as (a|b| + |a|b) / (2 (|a| + |b|)).  The two products are rounded separately (no FMA
+// contraction), so for ab < 0 they cancel exactly and for ab > 0 the numerator is 2 round(ab);
+// +1e-300 keeps 0/0 out (it changes no quotient with |a| + |b| > 1e-284).
+__device__ __forceinline__ double psi_half_vl_sf(double a, double b) {
+    const double num = __dadd_rn(__dmul_rn(fabs(a), b), __dmul_rn(a, fabs(b)));
+    return num * (0.5 * rcp_nr((fabs(a) + fabs(b)) + 1e-300));
+}
+
 // NEXT-4 limiters (R-31; the paper fixes van Leer, L299-300) as slope limiters psi(a, b) =
 // phi(a/b) b for ab > 0, with A = |a|, B = |b| and the sign of b:
 //   minmod   m = A <= B ? A : B

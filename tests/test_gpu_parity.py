@@ -265,10 +265,15 @@ def _stream(w, mode=oracle.MODE_DOUBLE):
     return _check(w, mode=mode, kernel=pb.KERNEL_STREAM)
 
 
+@pytest.fixture
+def plain_stream(monkeypatch):
+    monkeypatch.setenv("PBE_TEMPORAL_BLOCK", "0")     # steps mode without temporal blocking
+
+
 @pytest.mark.parametrize("N", [4000, 4001, 20000])
-def test_stream_c4_steps_mode(N):
+def test_stream_c4_steps_mode(N, plain_stream):
     g, o = _stream(W.c4_sweep(N, batch=3, n_steps=120))
-    assert g["info"]["kernel"] == 3
+    assert g["info"]["kernel"] == 3 and g["info"]["steps_per_pass"] == 1
 
 
 def test_stream_landing_and_temperature_profile():
@@ -348,7 +353,8 @@ def temporal_blocking(monkeypatch):
     monkeypatch.setenv("PBE_TEMPORAL_BLOCK", "1")     # read by pbe_create
 
 
-@pytest.mark.parametrize("N,batch,steps", [(4000, 3, 7), (4000, 3, 8), (9001, 2, 61), (30000, 5, 100)])
+@pytest.mark.parametrize("N,batch,steps", [(4000, 3, 7), (4000, 3, 8), (9001, 2, 61), (30000, 5, 100),
+                                           (70001, 2, 19), (200003, 2, 17)])   # tiles 512 / 1024 / 2048
 def test_temporal_blocking_matches_oracle(N, batch, steps, temporal_blocking):
     import paper_2411_00742_b200 as pb
     g, o = _check(W.c4_sweep(N, batch=batch, n_steps=steps), kernel=pb.KERNEL_STREAM)

@@ -375,11 +375,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
     struct LanePart { double c, t, mu3p, dt, gacc; };
     // static shared arrays (direct LDS/STS; a pointer carved out of the dynamic buffer makes the
     // compiler form generic addresses, rematerialised every step)
+    // (primal-only variants keep no tangent part: every .d is 0 and small CTAs stay small, so
+    // many fit per SM)
     __shared__ WarpPart s_wp[MAXT / 32];
-    __shared__ LanePart s_lp[MAXT];
+    __shared__ LanePart s_lp[P > 0 ? MAXT : 1];
     auto load_ls = [&]() -> LaneScal {
         const WarpPart w = s_wp[warp];
-        const LanePart l = s_lp[tid];
+        const LanePart l = P > 0 ? s_lp[tid] : LanePart{0.0, 0.0, 0.0, 0.0, 0.0};
         LaneScal L;
         L.c = mk(w.c, l.c); L.t = mk(w.t, l.t); L.mu3p = mk(w.mu3p, l.mu3p); L.dt = mk(w.dt, l.dt);
         L.loss = w.loss; L.gacc = l.gacc; L.rms_c = w.rms_c; L.rms_L = w.rms_L; L.tn = w.tn;
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         if (lane == 0)
             s_wp[warp] = WarpPart{L.c.v, L.t.v, L.mu3p.v, L.dt.v, L.loss, L.rms_c, L.rms_L, L.tn, L.nstep, L.m,
                                   L.status, L.landing};
-        s_lp[tid] = LanePart{L.c.d, L.t.d, L.mu3p.d, L.dt.d, L.gacc};
+        if (P > 0) s_lp[tid] = LanePart{L.c.d, L.t.d, L.mu3p.d, L.dt.d, L.gacc};
     };
     const int pl = lane < nl ? lane : -1;                      // this lane's tangent within the group
     const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, pl >= 0 ? lane0 + pl : -1, kp.n_params,

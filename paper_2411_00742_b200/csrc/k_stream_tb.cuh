@@ -157,7 +157,11 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
     }
 }
 
+#if PBE_TB_MAXNREG
+__global__ void __maxnreg__(PBE_TB_MAXNREG) k_stream_tb(const StreamTBParams sp) {
+#else
 __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTBParams sp) {
+#endif
     constexpr int KB = TB_KB, GH = TB_GH, NWC = TB_NWC, K = 4;
     const KParams& kp = sp.kp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -188,6 +188,30 @@ def test_c5_full_size_sampled_sims():
     _cmp_tangents(gs, o)
 
 
+def test_c4_full_size_sampled_sims():
+    """C4 exactly as bench.py's secondary/next4 entries run it (64 x 10^6 bins, 1000 uncapped CFL
+    steps, temporal blocking by default): final records and distributions of 2 sampled sims
+    against the oracle (results never depend on the batch)."""
+    import torch
+
+    import paper_2411_00742_b200 as pb
+    w = W.c4_sweep(1_000_000, batch=64, n_steps=1000)
+    ctx = pb.context_for(w)
+    n0 = torch.from_numpy(np.ascontiguousarray(w.n0)).cuda()
+    nf = torch.empty((64, w.N), dtype=torch.float64, device="cuda")
+    ctx.run_batch(n0, w.c0, None, None, nf)
+    r = ctx.moments()
+    assert ctx.last_run_info()["steps_per_pass"] == 8
+    ctx.close()
+    assert np.all(r["status"] == 0) and np.all(r["steps"] == 1000)
+    sims = [0, 41]
+    o = oracle.run(w.subset(sims), threads=2)
+    g = dict(samples=r["moments"][sims], n_final=nf[sims].cpu().numpy(), status=r["status"][sims],
+             steps=r["steps"][sims])
+    _cmp_samples(g, o)
+    _cmp_n(g, o)
+
+
 # ---------------------------------------------------------------------------------------
 # edge cases
 # ---------------------------------------------------------------------------------------

@@ -163,3 +163,21 @@ def test_adjoint_rejects_bad_arguments():
     with pytest.raises(pb.PBEError):
         ctx.adjoint_gradient(w.n_params)                                   # no adjoint run yet
     ctx.close()
+
+
+def test_adjoint_full_size_matches_gpu_tangents():
+    """NEXT-3 exactly as bench.py times it (9 experiments, N = 2000, 12,000 steps, 1000 POLY
+    coefficients): the adjoint gradient of coefficients 0..9 and 990..999 against forward-mode
+    tangent lanes on the same parameters (the tangent path is itself pinned to the oracle)."""
+    import paper_2411_00742_b200 as pb
+    w = W.next3_estimation(n_params=1000)
+    g, rec, _ = gpu_adjoint(w)
+    assert (rec["status"] == 0).all()
+    Q = w.sol.shape[0]
+    for js in (np.arange(10), np.arange(990, 1000)):
+        seed = np.zeros((10, 1000 + Q))
+        seed[np.arange(10), js] = 1.0
+        r = pb.run_workload(W.replace(w, n_tangents=10, tangent_seed=seed), want_n=False)
+        scale = np.max(np.abs(g["grad"]), axis=1)
+        err = np.abs(g["grad"][:, js] - r["grad"]) / scale[:, None]
+        assert err.max() <= RTOL_GRAD, err.max()

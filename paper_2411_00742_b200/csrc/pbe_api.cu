@@ -742,6 +742,13 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     }
     int kind = cf.kernel;
     if (kind == PBE_KERNEL_AUTO) kind = rv ? PBE_KERNEL_RESIDENT : (cv ? PBE_KERNEL_CLUSTER : PBE_KERNEL_STREAM);
+    // uncapped-CFL steps mode, primal: temporal blocking in k_stream beats the cluster kernel on
+    // large meshes and large batches (measured: 1e5 x 64 2.38e11 vs 1.01e11, 1e4 x 1184 1.82e11
+    // vs 1.56e11, 1e5 x 1 1.81e10 vs 1.59e10; cluster wins at 3e4 x 64 and 1e4 x 64)
+    const bool tb_ok = ctx->temporal_block && steps_mode && cf.dt_fixed == 0.0 && std::isinf(cf.dt_max) && P == 0;
+    if (cf.kernel == PBE_KERNEL_AUTO && kind == PBE_KERNEL_CLUSTER && tb_ok && sv &&
+        (N >= 65536 || (long long)n_sims * N >= 8000000LL))
+        kind = PBE_KERNEL_STREAM;
     if (kind == PBE_KERNEL_CLUSTER && !cv)
         return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit a 16-CTA cluster", N, P);
     if (two_d) kind = PBE_KERNEL_2D;

@@ -336,6 +336,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         }
     };
     // moment KM partials of all V variables, warp-reduced into s_red[q][warp][KM][*]
+    // mu3 weights dL L_i^3 of this thread's bins, computed once (same formula as below, so the
+    // per-step moments are bitwise those of the on-the-fly weights); [K][NT] after the halo
+    double* s_w3 = s_halo + 2 * HP;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double Lc = fma((double)(i0 + k), kp.dL, L_half);
+        s_w3[k * NT + tid] = ((kp.dL * Lc) * Lc) * Lc;
+    }
     auto moment_partials = [&](int q, auto kmc) {
         constexpr int KM = decltype(kmc)::value;
         double acc[V];
@@ -343,10 +351,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
         for (int v = 0; v < V; ++v) acc[v] = 0.0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const double Lc = fma((double)(i0 + k), kp.dL, L_half);   // bin centre
-            double w = kp.dL;
+            double w;
+            if (KM == 3) w = s_w3[k * NT + tid];
+            else {
+                const double Lc = fma((double)(i0 + k), kp.dL, L_half);   // bin centre
+                w = kp.dL;
 #pragma unroll
-            for (int e = 0; e < KM; ++e) w *= Lc;
+                for (int e = 0; e < KM; ++e) w *= Lc;
+            }
 #pragma unroll
             for (int v = 0; v < V; ++v) acc[v] = fma(w, x[v][k], acc[v]);
         }

@@ -111,7 +111,10 @@ struct ResidentVariant {
 };
 // dynamic smem: halo (2 parities); the scalar state (WarpPart, LanePart) and the kinetics
 // tables are static shared arrays (<= 48 KB), accounted for by the 200 KB dynamic cap below
-size_t resident_smem(const ResidentVariant& v, int nt) { return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double); }
+size_t resident_smem(const ResidentVariant& v, int nt) {
+    return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double)      // halo, 2 parities
+           + (size_t)v.K * nt * sizeof(double);                        // mu3 weights [K][NT]
+}
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {

@@ -174,9 +174,11 @@ pbe_status pbe_tangents(pbe_ctx ctx, double* tangents, double* grad, int32_t on_
  * landing, dt cap, clip), derivatives equal to pbe_tangents' up to rounding.
  *   n0, n0_stride, n0_on_device, c0, t_samples: as pbe_run_batch
  *   target            host [n_sims][n_samples][2] (required: the loss R-23 is differentiated)
- *   checkpoint_every  store the distribution every K steps (0: K = ceil(sqrt(max_steps)));
- *                     device memory per simulation = 8 B x (16 max_steps
- *                     + N ceil(max_steps / K) + N (K + 1)) -- max_steps bounds the trace
+ *   checkpoint_every  store the distribution every K steps (0: K = ceil(sqrt(max_steps))); K is
+ *                     capped so that a segment's trace rows (and, when they fit, its K + 1
+ *                     states) are staged in shared memory; device memory per simulation =
+ *                     8 B x (16 max_steps + N ceil(max_steps / K) [+ N (K + 1) if the states
+ *                     do not fit shared memory]) -- max_steps bounds the trace
  * Restrictions (PBE_ERR_ARG): 1D model, sample mode (n_steps = 0), N <= 6144, n_params <=
  * 16 x the CTA size.  The gradient is w.r.t. theta only (not the solubility parameters).
  * Records, status, steps and loss of the forward pass are read with pbe_moments. */

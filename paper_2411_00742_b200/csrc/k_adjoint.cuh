@@ -41,6 +41,15 @@
 
 namespace pbe {
 
+#if PBE_TIMING
+__device__ unsigned long long g_adj_cycles[8];    // forward, recompute, backward-vector, backward-scalar
+#define PBE_ATS(v) long long v = clock64()
+#define PBE_ATA(i, a, b) t_acc[i] += (unsigned long long)((b) - (a))
+#else
+#define PBE_ATS(v)
+#define PBE_ATA(i, a, b)
+#endif
+
 constexpr int ADJ_TR = 16;        // doubles per step in the scalar trace
 constexpr int ADJ_GMAX = 16;      // dL/dtheta accumulators per thread
 enum AdjTrace {
@@ -59,6 +68,7 @@ struct AdjParams {
     double* gtheta;       // [S][n_params]
     long long n_ck;       // checkpoint slots per simulation
     int Kseg;
+    int seg_smem;         // 1: the segment states live in shared memory (seg unused)
 };
 
 // dG/dtheta_j at (S, T) in closed form (the parameters enter the laws of growth_rate as
@@ -88,6 +98,9 @@ __device__ __forceinline__ double dG_dtheta(const KParams& kp, const double* __r
 template <int K>
 __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const KParams& kp = ap.kp;
+#if PBE_TIMING
+    unsigned long long t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
     const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
     const int N = kp.N, NP = NT * K + 4;
@@ -97,11 +110,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const int Kseg = ap.Kseg;
     double* trs = ap.tr + (size_t)s * kp.max_steps * ADJ_TR;
     double* cks = ap.ck + (size_t)s * ap.n_ck * N;
-    double* sgs = ap.seg + (size_t)s * (Kseg + 1) * N;
-
     extern __shared__ double sm[];
     double* nb = sm;                      // [2][NP] states, bin i at [i + 2]
     double* lb = sm + 2 * NP;             // [2][NP] adjoints
+    // segment states n^{k0..k1}: shared memory when they fit (host decides), else global
+    double* sgs = ap.seg_smem ? sm + 4 * NP : ap.seg + (size_t)s * (Kseg + 1) * N;
+    // the segment's trace rows, staged in shared memory at every segment start
+    double* s_trs = sm + 4 * NP + (ap.seg_smem ? (size_t)(Kseg + 1) * N : 0);
     __shared__ double s_red[32][4];
     __shared__ double s_sc[12];
     __shared__ int s_go, s_sample, s_bad, s_ok;
@@ -191,8 +206,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     int m = 0, status = ST_OK;
     bool landing = false;
     // kinetics of the step from (c, t) + its linearisation (lane 0: dc, lane 1: dt, lane 2: dG)
+    const KinCache KC = kin_cache(kp, KL, kT);           // constant: theta, solubility, knots
+    double tn_c = kp.t_samples[0];                         // t_samples[m], read once per sample
     auto kinetics = [&](long long k) -> bool {
-        const KinCache KC = kin_cache(kp, KL, kT);
         const D1 cD = mk(c, lane == 0 ? 1.0 : 0.0), tD = mk(t, lane == 1 ? 1.0 : 0.0);
         D1 T;
         const D1 S = supersaturation(kp, KL, kT, KC, tD, cD, T);
@@ -200,7 +216,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                    ? poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S)   // warp-cooperative
                    : growth_rate(kp, KL, S, T);
         if (lane == 2) G = mk(G.v, 1.0);
-        const double tn = kp.t_samples[m];
+        const double tn = tn_c;
         const StepScalars sc = time_step(kp, G, tD, tn, false);
         if (sc.err != ST_OK) { status = sc.err; return false; }
         const D1 tp = sc.landing ? mk(tn) : tD + sc.dt;
@@ -250,6 +266,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     // ---- forward pass: checkpoints + trace -------------------------------------------------------
     int q = 0;
     long long k = 0;
+    PBE_ATS(tf0);
     while (s_go) {
         if (k % Kseg == 0) {
             double* ckp = cks + (size_t)(k / Kseg) * N;
@@ -285,7 +302,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                         tr[TR_L1] = gL / mu0;
                     }
                 }
-                if (landing) ++m;
+                if (landing) { ++m; if (m < kp.M) tn_c = kp.t_samples[m]; }
                 if (m >= kp.M) go = false;
                 else if (nstep >= kp.max_steps) { status = ST_MAXSTEPS; go = false; }
                 else go = kinetics(k + 1);
@@ -296,6 +313,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         q ^= 1;
         ++k;
     }
+    PBE_ATS(tf1);
+    PBE_ATA(0, tf0, tf1);
     if (warp == 0 && lane == 0) {
         kp.status[s] = status;
         kp.steps[s] = nstep;
@@ -331,8 +350,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     };
     // warp-0 adjoint scalars: of c^{k+1} (before the sample term of step k), t^{k+1}, mu3p^{k+1}
     double lam_c = 0.0, lam_t = 0.0, lam_mu = 0.0;
+    long long k0s = 0;                             // first step of the staged trace segment
     auto pre_step = [&](long long kk) {            // warp 0: broadcast what the vector phase of kk needs
-        const double* r = trs + (size_t)kk * ADJ_TR;
+        const double* r = s_trs + (size_t)(kk - k0s) * ADJ_TR;
         const double lcp = lam_c + r[TR_LC];
         if (lane == 0) {
             s_sc[SC_LM] = -rho * lcp + lam_mu;     // adjoint of mu3(n^{kk+1})
@@ -346,7 +366,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const long long nseg = (Ktot + Kseg - 1) / Kseg;
     for (long long sg = nseg - 1; sg >= 0; --sg) {
         const long long k0 = sg * Kseg, k1 = min(k0 + (long long)Kseg, Ktot);
+        // stage the segment's trace rows (read by every step below)
+        __syncthreads();                                       // previous segment's readers are done
+        for (int e = tid; e < (int)(k1 - k0) * ADJ_TR; e += NT) s_trs[e] = __ldcg(trs + (size_t)k0 * ADJ_TR + e);
+        k0s = k0;
+        __syncthreads();
         // re-march the segment from its checkpoint (C^k from the trace): states n^{k0..k1}
+        PBE_ATS(tr0);
         {
             const double* ckp = cks + (size_t)sg * N;
 #pragma unroll
@@ -357,7 +383,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                 double* sp = sgs + (size_t)(kk - k0) * N;
 #pragma unroll
                 for (int j = 0; j < K; ++j) if (i0 + j < N) sp[i0 + j] = nb[qq * NP + i0 + j + 2];
-                const double* r = trs + (size_t)kk * ADJ_TR;
+                const double* r = s_trs + (size_t)(kk - k0) * ADJ_TR;
                 update(qq, r[TR_C], r[TR_KAP2], clip);
                 __syncthreads();
                 qq ^= 1;
@@ -368,7 +394,10 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         }
         if (warp == 0) pre_step(k1 - 1);
         __syncthreads();
+        PBE_ATS(tr1);
+        PBE_ATA(1, tr0, tr1);
         for (long long kk = k1 - 1; kk >= k0; --kk) {
+            PBE_ATS(tb0);
             // ---- vector phase: lambda^{kk+1} (+ mass-balance and sample terms, clip marks) ->
             //      lambda^kk, partial lambda_C -------------------------------------------------
             if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
@@ -431,9 +460,11 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             for (int off = 16; off > 0; off >>= 1) lamC += __shfl_xor_sync(0xffffffffu, lamC, off);
             if (lane == 0) s_red[warp][0] = lamC;
             __syncthreads();
+            PBE_ATS(tb1);
+            PBE_ATA(2, tb0, tb1);
             // ---- scalar phase (warp 0): adjoints of c^kk, t^kk, mu3p^kk; lambda_G^kk ------------
             if (warp == 0) {
-                const double* r = trs + (size_t)kk * ADJ_TR;
+                const double* r = s_trs + (size_t)(kk - k0) * ADJ_TR;
                 const double LC = block_total(0);
                 const double lcp = lam_c + r[TR_LC];
                 const double nc = lcp + LC * r[TR_CC] + lam_t * r[TR_TC];
@@ -448,6 +479,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             lg_prev = s_sc[SC_LG]; S_prev = s_sc[SC_S]; T_prev = s_sc[SC_T];
             have_lg = true;
             ql ^= 1;
+            PBE_ATS(tb2);
+            PBE_ATA(3, tb1, tb2);
         }
         __syncthreads();
     }
@@ -457,6 +490,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         const int j = tid + g * NT;
         if (j < kp.n_params) ap.gtheta[(size_t)s * kp.n_params + j] = gacc[g];
     }
+#if PBE_TIMING
+    if (blockIdx.x == 0 && tid == 0) { t_acc[4] = (unsigned long long)Ktot; for (int i = 0; i < 8; ++i) g_adj_cycles[i] = t_acc[i]; }
+#endif
 }
 
 }  // namespace pbe

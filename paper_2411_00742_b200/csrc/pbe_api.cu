@@ -585,6 +585,9 @@ const char* pbe_version(void) { return "libpbe 0.1 (sm_100a)"; }
 int pbe_debug_phase_cycles(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, pbe::g_phase_cycles, sizeof(pbe::g_phase_cycles)) == cudaSuccess ? 0 : 1;
 }
+int pbe_debug_adjoint_cycles(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, pbe::g_adj_cycles, sizeof(pbe::g_adj_cycles)) == cudaSuccess ? 0 : 1;
+}
 #endif
 
 const char* pbe_last_error(pbe_ctx ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
@@ -900,12 +903,27 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     if (ctx->n_params > nt * pbe::ADJ_GMAX)
         return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: %d parameters exceed %d for N = %d", ctx->n_params, nt * pbe::ADJ_GMAX, N);
     const long long ms = cf.max_steps;
+    // segment length: the segment's trace rows are staged in shared memory every segment, and
+    // its states n^{k0..k1} live there too when they fit (else in a global buffer)
+    const size_t smem_cap = 220 * 1024, row = (size_t)N * sizeof(double), trow = pbe::ADJ_TR * sizeof(double);
     int Kseg = checkpoint_every;
     if (Kseg == 0) Kseg = std::max(8, (int)std::ceil(std::sqrt((double)ms)));       // O(sqrt) memory
+    int seg_smem = 0;
+    {
+        // largest K' <= Kseg with the states in shared memory; take it when K' >= min(Kseg, 4)
+        long long kfit = ((long long)smem_cap - (long long)smem - (long long)row) / (long long)(row + trow);
+        if (kfit >= std::min(Kseg, 4)) { Kseg = (int)std::min<long long>(Kseg, kfit); seg_smem = 1; }
+        else {
+            const long long ktr = ((long long)smem_cap - (long long)smem) / (long long)trow;   // trace only
+            if (ktr < 1) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: no shared memory left for the trace");
+            Kseg = (int)std::min<long long>(Kseg, ktr);
+        }
+    }
+    smem += (size_t)Kseg * trow + (seg_smem ? (size_t)(Kseg + 1) * row : 0);
     const long long n_ck = (ms + Kseg - 1) / Kseg;
     const size_t tr_b = (size_t)n_sims * ms * pbe::ADJ_TR * sizeof(double);
     const size_t ck_b = (size_t)n_sims * n_ck * N * sizeof(double);
-    const size_t sg_b = (size_t)n_sims * (Kseg + 1) * N * sizeof(double);
+    const size_t sg_b = seg_smem ? sizeof(double) : (size_t)n_sims * (Kseg + 1) * N * sizeof(double);
     if ((double)tr_b + ck_b + sg_b > 64.0 * (1ull << 30))
         return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: trace + checkpoints need %.1f GB (> 64 GB): lower max_steps or n_sims",
                     ((double)tr_b + ck_b + sg_b) / (1ull << 30));
@@ -924,7 +942,7 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     ap.kp = make_kparams(ctx, n_sims, n0_dev, n0_stride, target, nullptr, nullptr, 1);
     ap.kp.P = 0;
     ap.ck = ctx->ack.as<double>(); ap.seg = ctx->aseg.as<double>(); ap.tr = ctx->atr.as<double>();
-    ap.gtheta = ctx->agrad.as<double>(); ap.n_ck = n_ck; ap.Kseg = Kseg;
+    ap.gtheta = ctx->agrad.as<double>(); ap.n_ck = n_ck; ap.Kseg = Kseg; ap.seg_smem = seg_smem;
     CUDA_TRY(ctx, cudaFuncSetAttribute(av->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ctx->info = pbe_run_info{};
     void* args[] = {&ap};

@@ -69,6 +69,7 @@ struct TBTile {
     double C, clip, dL, L_half;
     int lim;
     unsigned long long* empty;   // stage's empty barrier
+    double* w3s;                 // smem [NWC][KW][32]: mu3 weights of the lanes' cells
 };
 
 template <int KW, bool NEG, int LK>
@@ -78,7 +79,8 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
     const int SEG = T.TB / NWC;
     const int x0 = warp * SEG + lane * KW;                      // window index of the lane's first cell
     const double C = T.C, aC = fabs(C), kap2 = aC * (1.0 - aC);
-    double c[KW], w3[KW];
+    double c[KW];
+    double* w3 = T.w3s + (size_t)warp * KW * 32 + lane;         // [k][lane]: conflict-free
     unsigned dom = 0, own = 0;
 #pragma unroll
     for (int k = 0; k < KW; ++k) {
@@ -89,7 +91,7 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
         dom |= (in ? 1u : 0u) << k;
         own |= (ow ? 1u : 0u) << k;
         const double Lc = fma((double)i, T.dL, T.L_half);
-        w3[k] = ow ? T.dL * Lc * Lc * Lc : 0.0;                 // mu3 weight (0 off the owned cells)
+        w3[k * 32] = ow ? T.dL * Lc * Lc * Lc : 0.0;            // mu3 weight (0 off the owned cells)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(T.empty);                        // this warp is done with the stage
@@ -125,7 +127,7 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
             bad |= o && v < -T.clip;
             v = (v < 0.0 && v >= -T.clip) ? 0.0 : v;            // round-off clip (R-17)
             c[k] = v;
-            a3 = fma(w3[k], v, a3);
+            a3 = fma(w3[k * 32], v, a3);
         }
         // this sub-step's warp partial (fixed-order xor tree); lane 0 writes [mu3, bad]
 #pragma unroll
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
                 const int lk = vl == LIM_VANLEER ? 1 : (vl == LIM_UPWIND ? 0 : 2);
                 TBTile tile{smem + (size_t)st * WL, (W.cur ? sp.buf0 : sp.buf1) + (size_t)s * sp.pitch + b0 + GH,
                             sp.part + (((size_t)s * sp.T_sim + j) * NWC + warp) * KB * 5, b0, nb, N, TB, W.depth,
-                            W.sample != 0, W.sign * kp.courant, W.clip, kp.dL, L_half, vl, &s_empty[st]};
+                            W.sample != 0, W.sign * kp.courant, W.clip, kp.dL, L_half, vl, &s_empty[st], work0};
                 const bool neg_c = W.sign < 0;
 #define PBE_TBW(KWV)                                                                                        \
     do {                                                                                                    \
@@ -273,7 +275,11 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
         else        { if (lk == 1) tb_tile_warp<KWV, true, 1>(tile); else if (lk == 0) tb_tile_warp<KWV, true, 0>(tile);   \
                       else tb_tile_warp<KWV, true, 2>(tile); }                                              \
     } while (0)
+#if PBE_TB_ONLY_VL9
+                if (!neg_c) tb_tile_warp<9, false, 1>(tile); else tb_tile_warp<9, true, 1>(tile);   // A/B only
+#else
                 if (TB == 2048) PBE_TBW(9); else if (TB == 1024) PBE_TBW(5); else PBE_TBW(3);
+#endif
 #undef PBE_TBW
             }
         }

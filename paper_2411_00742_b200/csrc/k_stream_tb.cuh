@@ -78,7 +78,7 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int SEG = T.TB / NWC;
     const int x0 = warp * SEG + lane * KW;                      // window index of the lane's first cell
-    const double C = T.C, aC = fabs(C), kap2 = aC * (1.0 - aC);
+    const double C = T.C, aC = fabs(C), kap2 = aC * (1.0 - aC), kh = 0.5 * kap2;
     double c[KW];
     double* w3 = T.w3s + (size_t)warp * KW * 32 + lane;         // [k][lane]: conflict-free
     unsigned dom = 0, own = 0;
@@ -111,10 +111,13 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
             const int u = NEG ? f : f - 1;
             const int ja = NEG ? f + 1 : f - 1;
             const double a = w[ja] - w[ja - 1], b = w[f] - w[f - 1];
-            double h = 0.0;
-            if (LK == 1) h = psi_half_vl_sf(a, b);
-            else if (LK == 2) h = psi_half(T.lim, a, b);
-            F[f - 2] = fma(C, w[u], kap2 * h);
+            if (LK == 1) {                                      // select-free van Leer, 1/2 folded into kap
+                const double num = __dadd_rn(__dmul_rn(fabs(a), b), __dmul_rn(a, fabs(b)));
+                F[f - 2] = fma(C, w[u], (kh * num) * rcp_nr((fabs(a) + fabs(b)) + 1e-300));
+            } else {
+                const double h = LK == 2 ? psi_half(T.lim, a, b) : 0.0;
+                F[f - 2] = fma(C, w[u], kap2 * h);
+            }
         }
         const bool last = q == T.d - 1;
         bool bad = false;

@@ -127,8 +127,8 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
             double v = w[k + 2] - (F[k + 1] - F[k]);
             v = ((dom >> k) & 1u) ? v : 0.0;                    // ghost cells outside [0, N) stay 0
             const bool o = (own >> k) & 1u;
-            bad |= o && v < -T.clip;
-            v = (v < 0.0 && v >= -T.clip) ? 0.0 : v;            // round-off clip (R-17)
+            bad |= o && v < -T.clip;                            // status NEG: the stored value is moot
+            v = fmax(v, 0.0);                                   // round-off clip (R-17)
             c[k] = v;
             a3 = fma(w3[k * 32], v, a3);
         }

@@ -310,10 +310,13 @@ def main():
             # 2D: the fused kernel reads + writes each cell once per split step (16 B); the unfused
             # one (PBE_2D_UNFUSED=1) does that once per sweep (32 B)
             unfused = info["kernel"] == pb.KERNEL_2D and os.environ.get("PBE_2D_UNFUSED", "0") not in ("", "0")
-            bytes_per = 16.0 * (1 + P) * (2.0 if unfused else 1.0)
+            spp = max(1, int(info.get("steps_per_pass", 1)))       # temporal blocking: 16 B per spp steps
+            bytes_per = 16.0 * (1 + P) * (2.0 if unfused else 1.0) / spp
             achieved = bytes_per * bu_local / (kms * 1e-3) / 1e9
             hbm = float(peaks.get("hbm_gbs", 6650.0))
             kname = ("k_2d" if unfused else "k_2d_fused") if info["kernel"] == pb.KERNEL_2D else "k_stream"
+            if spp > 1:
+                kname = "k_stream_tb"
             r = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm, traffic=None,
                      kernel=kname, bytes_per_bin_update=bytes_per,
                      peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s", kernel_ms=kms)
@@ -326,6 +329,11 @@ def main():
                      kernel="k_cluster" if info["kernel"] == pb.KERNEL_CLUSTER else "k_resident",
                      flops_per_bin_update=f,
                      peak_source=f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {sm_max:.0f} MHz", kernel_ms=kms)
+        if r.get("kernel") == "k_stream_tb":
+            # temporal blocking moves 16 B per bin per HBM pass of spp steps, so HBM is not its bound;
+            # report where it stands against the plain-streaming ceiling as well
+            r["note"] = "temporal blocking: traffic 16 B / steps_per_pass; latency/FP64-bound, not HBM-bound"
+            r["frac_of_plain_stream_ceiling"] = bu_local / (kms * 1e-3) / (r["peak"] * 1e9 / 16.0)
         # DRAM bytes of the kernel from an ncu --set full capture (profiles/traffic.json), as
         # bytes per bin-update, scaled to this launch
         prof = os.path.join(ROOT, "profiles", "traffic.json")

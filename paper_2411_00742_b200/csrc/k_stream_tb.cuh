@@ -72,7 +72,7 @@ struct TBTile {
     double* w3s;                 // smem [NWC][KW][32]: mu3 weights of the lanes' cells
 };
 
-template <int KW, bool NEG, int LK>
+template <int KW, bool NEG, int LK, bool INT>      // INT: the warp's region lies inside [0, N)
 __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
     constexpr int KB = TB_KB, GH = TB_GH, NWC = TB_NWC;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -125,7 +125,7 @@ __device__ __forceinline__ void tb_tile_warp(const TBTile& T) {
 #pragma unroll
         for (int k = 0; k < KW; ++k) {
             double v = w[k + 2] - (F[k + 1] - F[k]);
-            v = ((dom >> k) & 1u) ? v : 0.0;                    // ghost cells outside [0, N) stay 0
+            if (!INT) v = ((dom >> k) & 1u) ? v : 0.0;          // ghost cells outside [0, N) stay 0
             const bool o = (own >> k) & 1u;
             bad |= o && v < -T.clip;                            // status NEG: the stored value is moot
             v = fmax(v, 0.0);                                   // round-off clip (R-17)
@@ -271,15 +271,22 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
                             sp.part + (((size_t)s * sp.T_sim + j) * NWC + warp) * KB * 5, b0, nb, N, TB, W.depth,
                             W.sample != 0, W.sign * kp.courant, W.clip, kp.dL, L_half, vl, &s_empty[st], work0};
                 const bool neg_c = W.sign < 0;
+                // this warp's register region [b0 - GH + w SEG, + SEG + 2 GH) inside the domain?
+                const int rg0 = b0 - GH + warp * (TB / NWC);
+                const bool inside = rg0 >= 0 && rg0 + TB / NWC + 2 * GH <= N;
 #define PBE_TBW(KWV)                                                                                        \
     do {                                                                                                    \
-        if (!neg_c) { if (lk == 1) tb_tile_warp<KWV, false, 1>(tile); else if (lk == 0) tb_tile_warp<KWV, false, 0>(tile); \
-                      else tb_tile_warp<KWV, false, 2>(tile); }                                             \
-        else        { if (lk == 1) tb_tile_warp<KWV, true, 1>(tile); else if (lk == 0) tb_tile_warp<KWV, true, 0>(tile);   \
-                      else tb_tile_warp<KWV, true, 2>(tile); }                                              \
+        if (lk == 1) {                                                                                      \
+            if (inside) { if (!neg_c) tb_tile_warp<KWV, false, 1, true>(tile); else tb_tile_warp<KWV, true, 1, true>(tile); } \
+            else        { if (!neg_c) tb_tile_warp<KWV, false, 1, false>(tile); else tb_tile_warp<KWV, true, 1, false>(tile); } \
+        } else if (lk == 0) {                                                                               \
+            if (!neg_c) tb_tile_warp<KWV, false, 0, false>(tile); else tb_tile_warp<KWV, true, 0, false>(tile); \
+        } else {                                                                                            \
+            if (!neg_c) tb_tile_warp<KWV, false, 2, false>(tile); else tb_tile_warp<KWV, true, 2, false>(tile); \
+        }                                                                                                   \
     } while (0)
 #if PBE_TB_ONLY_VL9
-                if (!neg_c) tb_tile_warp<9, false, 1>(tile); else tb_tile_warp<9, true, 1>(tile);   // A/B only
+                if (!neg_c) tb_tile_warp<9, false, 1, false>(tile); else tb_tile_warp<9, true, 1, false>(tile);   // A/B only
 #else
                 if (TB == 2048) PBE_TBW(9); else if (TB == 1024) PBE_TBW(5); else PBE_TBW(3);
 #endif

@@ -181,25 +181,15 @@ __device__ __forceinline__ D1 poly_long_warp_seeded(const double* __restrict__ a
     double q = 0.0, dq = 0.0, sp[PP];
 #pragma unroll
     for (int p = 0; p < PP; ++p) sp[p] = 0.0;
-    for (int i0 = ((m - 1) >> 2) << 2; i0 >= 0; i0 -= 4) {      // blocks of 4, loads ahead of the chains
-        double av[4], sv[4][PP];
+    for (int i = m - 1; i >= 0; --i) {
+        const int j = j0 + i;
+        const bool on = j < n;
+        const double aj = on ? __ldg(a + j) : 0.0;
+        dq = fma(dq, x, q);
+        q = fma(q, x, aj);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = j0 + i0 + u;
-            const bool on = i0 + u < m && j < n;
-            av[u] = on ? __ldg(a + j) : 0.0;
-#pragma unroll
-            for (int p = 0; p < PP; ++p) sv[u][p] = (on && p < nl) ? __ldg(seed + (size_t)(lane0 + p) * nsd + j) : 0.0;
-        }
-#pragma unroll
-        for (int u = 3; u >= 0; --u) {
-            if (i0 + u < m) {
-                dq = fma(dq, x, q);
-                q = fma(q, x, av[u]);
-#pragma unroll
-                for (int p = 0; p < PP; ++p) sp[p] = fma(sp[p], x, sv[u][p]);
-            }
-        }
+        for (int p = 0; p < PP; ++p)
+            sp[p] = fma(sp[p], x, (on && p < nl) ? __ldg(seed + (size_t)(lane0 + p) * nsd + j) : 0.0);
     }
     const double xl = pow(x, (double)j0), xl1 = xl * x;   // x^(l m), x^(l m + 1)
     double t = xl1 * q;

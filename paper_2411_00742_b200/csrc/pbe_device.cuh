@@ -195,19 +195,11 @@ __device__ __forceinline__ D1 poly_long_warp(const double* __restrict__ a, int n
     const int m = (n + 31) >> 5;
     const int j0 = lane * m;
     double q = 0.0, dq = 0.0;
-    // Horner from i = m-1 down to 0, coefficients loaded 8 at a time ahead of the FMA chain
-    // (same operation order as the plain loop)
-    for (int i0 = ((m - 1) >> 3) << 3; i0 >= 0; i0 -= 8) {
-        double av[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int j = j0 + i0 + u;
-            av[u] = (i0 + u < m && j < n) ? __ldg(a + j) : 0.0;
-        }
-#pragma unroll
-        for (int u = 7; u >= 0; --u) {
-            if (i0 + u < m) { dq = fma(dq, x, q); q = fma(q, x, av[u]); }
-        }
+    for (int i = m - 1; i >= 0; --i) {
+        const int j = j0 + i;
+        const double aj = j < n ? __ldg(a + j) : 0.0;
+        dq = fma(dq, x, q);
+        q = fma(q, x, aj);
     }
     const double xl = pow(x, (double)j0);             // x^(l m)
     double t = xl * x * q;                             // x^(l m + 1) q(x)

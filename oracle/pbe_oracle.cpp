@@ -441,9 +441,11 @@ inline void run_one(const oracle_problem& pb, const BatchIO& io, int s, int mode
         std::vector<Dual> th, sol; seed_inputs<Dual>(pb, th_s, 0, 0, 0, th, sol);
         Result<Dual> R = simulate<Dual>(pbs, th.data(), sol.data(), n0, c0);
         for (int m = 0; m < Mr; ++m) for (int k = 0; k < 6; ++k) smp[m * 6 + k] = R.rec[m][k].v;
+        // unreached samples (R-26: a failed simulation's later records are NaN) have NaN tangents too
         if (io.tsamples)
             for (int m = 0; m < Mr; ++m) for (int p = 0; p < P; ++p) for (int k = 0; k < 5; ++k)
-                io.tsamples[(((size_t)s * Mr + m) * P + p) * 5 + k] = R.rec[m][k + 1].d[p];
+                io.tsamples[(((size_t)s * Mr + m) * P + p) * 5 + k] =
+                    std::isnan(R.rec[m][k + 1].v) ? R.rec[m][k + 1].v : R.rec[m][k + 1].d[p];
         io.status[s] = R.status; io.steps[s] = R.steps;
         if (io.n_final) for (int i = 0; i < N; ++i) io.n_final[(size_t)s * N + i] = R.n_final[i].v;
         if (io.ndot_final)
@@ -462,7 +464,8 @@ inline void run_one(const oracle_problem& pb, const BatchIO& io, int s, int mode
             }
             if (io.tsamples)
                 for (int m = 0; m < Mr; ++m) for (int k = 0; k < 5; ++k)
-                    io.tsamples[(((size_t)s * Mr + m) * P + p) * 5 + k] = R.rec[m][k + 1].imag() / h;
+                    io.tsamples[(((size_t)s * Mr + m) * P + p) * 5 + k] =
+                        std::isnan(R.rec[m][k + 1].real()) ? R.rec[m][k + 1].real() : R.rec[m][k + 1].imag() / h;
             if (io.ndot_final)
                 for (int i = 0; i < N; ++i) io.ndot_final[((size_t)s * P + p) * N + i] = R.n_final[i].imag() / h;
         }

@@ -1,0 +1,94 @@
+"""Seeded randomized parity: configuration combinations the targeted tests do not cross —
+mesh size, tangent lanes, the five limiters, the three growth laws (incl. long polynomials),
+both solubility forms, constant and ramped temperature, fixed / capped / uncapped time steps,
+sample and steps modes, Gaussian and log-normal seeds, and every 1D kernel (AUTO, resident,
+cluster, stream) — each against the oracle with the same bars as test_gpu_parity.py.
+Every case is drawn from numpy PCG64(seed) so failures reproduce exactly."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.test_gpu_parity import RTOL_TAN, _cmp_n, _cmp_samples, _cmp_tangents
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = (0, 1, 2, 3)     # AUTO, RESIDENT, CLUSTER, STREAM
+
+
+def random_case(seed):
+    rng = np.random.Generator(np.random.PCG64(1000 + seed))
+    kernel = int(rng.choice(KERNELS))
+    if kernel == 2:
+        N = int(rng.integers(3000, 9000))
+    elif kernel == 3:
+        N = int(rng.integers(300, 6000))
+    else:
+        N = int(rng.integers(3, 700))
+    P = int(rng.integers(0, 5 if kernel == 3 else (9 if kernel == 2 else 11)))
+    lim = int(rng.integers(0, 5))
+    law = int(rng.choice([W.LAW_CONST, W.LAW_ARRHENIUS, W.LAW_POLY]))
+    S = int(rng.integers(1, 4))
+    dL = 1200.0 / N
+    if law == W.LAW_CONST:
+        theta = np.full((S, 1), float(rng.uniform(-0.8, 2.0)))
+    elif law == W.LAW_ARRHENIUS:
+        base = np.array(W.ARRHENIUS_DEFAULT)[: (6 if rng.random() < 0.6 else 3)]
+        theta = base[None, :] * np.exp(0.1 * rng.standard_normal((S, base.shape[0])))
+    else:
+        k = int(rng.integers(1, 14))
+        theta = np.abs(rng.standard_normal((S, k))) * np.array([20.0 / (j + 1) for j in range(k)])[None, :]
+    sol_kind = int(rng.integers(0, 2))
+    sol = np.array(W.SOL_EXP_DEFAULT) if sol_kind == 0 else np.array([3.37, 0.07, 0.002])
+    if rng.random() < 0.5:
+        knot_t, knot_T = np.array([0.0]), np.full((S, 1), float(rng.uniform(10.0, 25.0)))
+    else:
+        knot_t = np.array([0.0, float(rng.uniform(5.0, 30.0)), float(rng.uniform(31.0, 60.0))])
+        knot_T = np.tile(np.array([[float(rng.uniform(10, 20)), float(rng.uniform(15, 25)), float(rng.uniform(10, 25))]]),
+                         (S, 1))
+    # concentration around saturation at the initial temperature: growth or dissolution
+    T0 = knot_T[0, 0]
+    csat = sol[0] * math.exp(sol[1] * T0) if sol_kind == 0 else sol[0] + sol[1] * T0 + sol[2] * T0 * T0
+    c0 = csat * rng.uniform(0.85, 1.4, S)
+    seed_fn = W.gaussian_seed if rng.random() < 0.6 else W.lognormal_seed
+    mean = float(rng.uniform(150.0, 900.0))
+    n0 = seed_fn(N, dL, mean=mean, sigma=float(rng.uniform(max(3 * dL, 20.0), 80.0)), m0=float(rng.uniform(0.2, 2.0)))
+    mode = rng.choice(["fixed", "capped", "uncapped"])
+    dt_fixed = float(rng.uniform(0.01, 0.3)) * dL if mode == "fixed" else 0.0
+    dt_max = float(rng.uniform(0.02, 0.5)) if mode == "capped" else math.inf
+    steps_mode = kernel == 3 and rng.random() < 0.5 or rng.random() < 0.2
+    t_max = float(rng.uniform(2.0, 30.0))
+    M = int(rng.integers(1, 12))
+    w = W.Workload(
+        name=f"fuzz{seed}", N=N, dL=dL, limiter=lim, dt_fixed=dt_fixed, dt_max=dt_max, max_steps=4000,
+        n_steps=int(rng.integers(20, 150)) if steps_mode else 0, law=law, theta=theta, sol_kind=sol_kind, sol=sol,
+        knot_t=knot_t, knot_T=knot_T, n0=n0[None, :], c0=c0,
+        t_samples=np.array([t_max]) if steps_mode else np.linspace(t_max / M, t_max, M),
+        target=None, n_tangents=P)
+    return w, kernel
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_matches_oracle(seed):
+    import paper_2411_00742_b200 as pb
+    w, kernel = random_case(seed)
+    mode = oracle.MODE_DUAL if w.n_tangents else oracle.MODE_DOUBLE
+    o = oracle.run(w, mode=mode, threads=4)
+    try:
+        g = pb.run_workload(w, kernel=kernel)
+    except pb.PBEError as e:            # only documented argument limits may refuse a case
+        pytest.skip(f"refused: {e}")
+    assert np.array_equal(g["status"], o["status"]), (g["status"], o["status"])
+    assert np.array_equal(g["steps"], o["steps"]), (g["steps"], o["steps"])
+    _cmp_samples(g, o)
+    _cmp_n(g, o)
+    if w.n_tangents:
+        _cmp_tangents(g, o)
+        for s in range(w.n_sims):
+            if o["status"][s] != 0:
+                continue
+            for p in range(w.n_tangents):
+                sc = np.max(np.abs(o["ndot_final"][s, p]))
+                assert np.max(np.abs(g["ndot_final"][s, p] - o["ndot_final"][s, p])) <= RTOL_TAN * max(sc, 1e-300)

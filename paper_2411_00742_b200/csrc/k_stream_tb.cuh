@@ -217,7 +217,16 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
         const double* pt = sp.part + (size_t)s * sp.T_sim * NWC * KB * 5;
         const int ne = sp.T_sim * NWC;
         double a = 0.0;
-        for (int e = lane; e < ne; e += 32) a += pt[((size_t)e * KB + q) * 5 + km];
+        constexpr int UB = 8;                                // 8 L2 round trips in flight, same order
+        int e = lane;
+        for (; e + 32 * (UB - 1) < ne; e += 32 * UB) {
+            double x[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) x[u] = pt[((size_t)(e + 32 * u) * KB + q) * 5 + km];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) a += x[u];
+        }
+        for (; e < ne; e += 32) a += pt[((size_t)e * KB + q) * 5 + km];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
         return a;

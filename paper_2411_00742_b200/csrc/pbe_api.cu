@@ -232,7 +232,8 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     int per_sm = 0;
     CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sv.fn, pbe::STREAM_NT, smem));
     if (per_sm < 1) return fail(ctx, PBE_ERR_CUDA, "k_stream does not fit on an SM (smem %zu)", smem);
-    per_sm = per_sm > 2 ? 2 : per_sm;
+    const int cap_sm = V == 1 && pbe::StreamCfg<1>::MINB > 2 ? pbe::StreamCfg<1>::MINB : 2;
+    per_sm = per_sm > cap_sm ? cap_sm : per_sm;
     const int G = per_sm * sms;
     const int T_sim = (N + TB - 1) / TB;
     const long long n_tiles = (long long)S * T_sim;
@@ -584,6 +585,9 @@ const char* pbe_version(void) { return "libpbe 0.1 (sm_100a)"; }
 // resident kernel's step phases measured by warp 0 of CTA 0.
 int pbe_debug_phase_cycles(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, pbe::g_phase_cycles, sizeof(pbe::g_phase_cycles)) == cudaSuccess ? 0 : 1;
+}
+int pbe_debug_stream_cycles(unsigned long long* out) {    // [1024][4], see k_stream.cuh
+    return cudaMemcpyFromSymbol(out, pbe::g_stream_cycles, sizeof(pbe::g_stream_cycles)) == cudaSuccess ? 0 : 1;
 }
 int pbe_debug_adjoint_cycles(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, pbe::g_adj_cycles, sizeof(pbe::g_adj_cycles)) == cudaSuccess ? 0 : 1;

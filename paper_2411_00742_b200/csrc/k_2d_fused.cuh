@@ -349,7 +349,21 @@ __global__ void __launch_bounds__(F2_NT, PBE_F2_MINB) k_2d_fused(const Params2DF
                 __threadfence();
                 double a[7] = {0, 0, 0, 0, 0, 0, 0};
                 const double* pt = p.part + (size_t)s * T2 * 7;
-                for (int b = tid; b < T2; b += F2_NT)
+                // UB tiles' partials in flight per L2 round trip; per-thread addition order unchanged
+                constexpr int UB = 4;
+                int b = tid;
+                for (; b + F2_NT * (UB - 1) < T2; b += F2_NT * UB) {
+                    double x[UB][7];
+#pragma unroll
+                    for (int u = 0; u < UB; ++u)
+#pragma unroll
+                        for (int k = 0; k < 7; ++k) x[u][k] = __ldcg(pt + (size_t)(b + F2_NT * u) * 7 + k);
+#pragma unroll
+                    for (int u = 0; u < UB; ++u)
+#pragma unroll
+                        for (int k = 0; k < 7; ++k) a[k] += x[u][k];
+                }
+                for (; b < T2; b += F2_NT)
 #pragma unroll
                     for (int k = 0; k < 7; ++k) a[k] += __ldcg(pt + (size_t)b * 7 + k);
 #pragma unroll

@@ -31,8 +31,9 @@ namespace pbe {
 
 #if PBE_TIMING
 // per CTA: own tile work (loop top -> CTA arrives at the grid barrier), grid-barrier wait,
-// scalar phase, steps (diagnostics builds only; tools/stream_cycles.py)
-__device__ unsigned long long g_stream_cycles[1024][4];
+// scalar phase, steps, warp-tiles that took the round-off clip path (diagnostics builds only;
+// tools/stream_cycles.py)
+__device__ unsigned long long g_stream_cycles[1024][5];
 #endif
 
 constexpr int STREAM_MAXS = 8;      // simulations one CTA may touch
@@ -452,6 +453,9 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
                 // round-off clip (R-17), rare: fix the stored values of this warp's bins
                 bool bad = false;
                 if (__any_sync(0xffffffffu, neg)) {
+#if PBE_TIMING
+                    if (lane == 0 && blockIdx.x < 1024) atomicAdd(&g_stream_cycles[blockIdx.x][4], 1ull);
+#endif
                     const double thr = s_clip[slot];
                     for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
                         for (int k = 0; k < K && g0 + k < nb; ++k) {

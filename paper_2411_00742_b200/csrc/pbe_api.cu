@@ -586,7 +586,7 @@ const char* pbe_version(void) { return "libpbe 0.1 (sm_100a)"; }
 int pbe_debug_phase_cycles(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, pbe::g_phase_cycles, sizeof(pbe::g_phase_cycles)) == cudaSuccess ? 0 : 1;
 }
-int pbe_debug_stream_cycles(unsigned long long* out) {    // [1024][4], see k_stream.cuh
+int pbe_debug_stream_cycles(unsigned long long* out) {    // [1024][5], see k_stream.cuh
     return cudaMemcpyFromSymbol(out, pbe::g_stream_cycles, sizeof(pbe::g_stream_cycles)) == cudaSuccess ? 0 : 1;
 }
 int pbe_debug_adjoint_cycles(unsigned long long* out) {

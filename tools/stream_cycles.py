@@ -20,9 +20,12 @@ r = pb.run_workload(w, want_n=False)
 info = r["info"]
 assert info["kernel"] == 3 and info["steps_per_pass"] == 1, info
 G = info["ctas"]
-buf = (C.c_ulonglong * (1024 * 4))()
+tile = 256
+while tile < 4096 and tile * 256 < N:      # stream_tile(N, 1), k_stream.cuh
+    tile *= 2
+buf = (C.c_ulonglong * (1024 * 5))()
 assert lib.pbe_debug_stream_cycles(buf) == 0
-a = np.array(buf, dtype=np.float64).reshape(1024, 4)[:G]
+a = np.array(buf, dtype=np.float64).reshape(1024, 5)[:G]
 st = a[:, 3]
 per = a[:, :3] / st[:, None]
 tot = per.sum(axis=1)
@@ -31,3 +34,5 @@ print(f"N {N} batch {B} steps {int(st.max())} CTAs {G}  main_ms {info['main_ms']
 for k, name in enumerate(["own tile work", "grid-barrier wait", "scalar phase"]):
     v = per[:, k]
     print(f"  {name:18s} mean {v.mean():8.0f}  min {v.min():8.0f}  max {v.max():8.0f}  ({100 * v.mean() / tot.mean():5.1f}%)")
+print(f"  clip-path warp-tiles per step (all CTAs) {a[:, 4].sum() / st.max():.1f} "
+      f"of {8 * np.ceil(N / tile) * B:.0f}")

@@ -10,11 +10,14 @@ import pytest
 LOG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2411_00742_b200",
                    "build_pbe.log")
 
-# mangled kernel -> max spill-store bytes (measured: C5 8 B, fused 2D 24-36 B, temporal blocking 124 B)
+# mangled kernel -> max spill-store bytes (measured: C5 8 B, fused 2D 24-36 B, temporal blocking 124 B,
+# plain streaming 80 B (scalar phase only), adjoint 0 B)
 LIMITS = {
     "_ZN3pbe10k_residentILi8ELi8ELi256ELb0ELi1EEEvNS_7KParamsE": 64,     # C5 (bench headline)
     "_ZN3pbe10k_2d_fusedENS_9Params2DFE": 96,                             # NEXT-1
     "_ZN3pbe11k_stream_tbENS_14StreamTBParamsE": 256,                     # NEXT-4 (C4 default)
+    "_ZN3pbe8k_streamILi0EEEvNS_12StreamParamsE": 160,                    # C4 plain streaming
+    "_ZN3pbe9k_adjointILi8EEEvNS_9AdjParamsE": 64,                        # NEXT-3
 }
 
 

@@ -129,7 +129,9 @@ const char* pbe_last_error(pbe_ctx ctx);
  *                piecewise linear through the knots, constant outside (R-14)
  *   tangent_seed host [n_tangents][n_params + n_sol] or NULL (= unit vectors e_0..e_{P-1}
  *                over theta).  Lane p differentiates along seed[p] (R-20).
- * Copied to the device (synchronously); the pointers are not retained. */
+ * Copied to the device (synchronously); the pointers are not retained.  If a run is still in
+ * flight, this call first waits for it (cudaStreamSynchronize of the last run's stream), so
+ * kinetics are never replaced under a running kernel. */
 pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t n_sims,
                             const double* theta, int32_t sol_kind, int32_t n_sol,
                             const double* sol_params, int32_t n_knots, const double* knot_t,
@@ -143,10 +145,12 @@ pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t 
  *   c0          host [n_sims] initial concentrations (>= 0)
  *   t_samples   host [n_samples] strictly increasing, > 0 (ignored in steps mode)
  *   target      host [n_sims][n_samples][2] = measured (c, mean length mu1/mu0) for the
- *               RSS loss (R-23), or NULL (no loss)
+ *               RSS loss (R-23), or NULL (no loss; must be NULL for the 2D model: PBE_ERR_ARG)
  *   n_final     device [n_sims][N] final distributions, or NULL
  *   ndot_final  device [n_sims][n_tangents][N] final tangent distributions, or NULL
- * Validates n0 only for shape/pointers (non-negativity of device n0 is the caller's). */
+ * Validates n0 only for shape/pointers (non-negativity of device n0 is the caller's).
+ * The context's input/output buffers are reused: a run enqueued on a different stream than
+ * the previous run first waits (cudaStreamWaitEvent) for the previous run's kernel. */
 pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride,
                          int32_t n0_on_device, const double* c0, const double* t_samples,
                          const double* target, double* n_final, double* ndot_final,

@@ -117,6 +117,24 @@ def _host(a, dtype=np.float64):
     return None if a is None else np.ascontiguousarray(a, dtype=dtype)
 
 
+def _check_dev(name: str, t, device: int, shapes) -> None:
+    """libpbe cannot check device buffers: a device tensor must be float64, contiguous, on the
+    context's device and of one of the allowed shapes (else out-of-bounds device accesses)."""
+    if t is None:
+        return
+    if isinstance(t, np.ndarray):
+        raise TypeError(f"{name}: expected a CUDA tensor, got a numpy array")
+    import torch
+    if t.dtype != torch.float64:
+        raise TypeError(f"{name}: dtype must be float64, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if t.device.type != "cuda" or t.device.index != device:
+        raise ValueError(f"{name}: must live on cuda:{device}, got {t.device}")
+    if tuple(t.shape) not in [tuple(s) for s in shapes]:
+        raise ValueError(f"{name}: shape {tuple(t.shape)} not in {[tuple(s) for s in shapes]}")
+
+
 class Context:
     """One libpbe context (pbe_create): a problem shape bound to one CUDA device."""
 
@@ -166,6 +184,12 @@ class Context:
         sol = _host(sol); knot_t = _host(np.atleast_1d(knot_t)); knot_T = _host(np.atleast_2d(knot_T))
         seed = _host(tangent_seed)
         per_sim = 1 if knot_T.shape[0] > 1 else 0
+        if knot_T.shape[0] not in (1, theta.shape[0]) or knot_T.shape[1] != knot_t.shape[0]:
+            raise ValueError(f"knot_T shape {knot_T.shape}: expected [1 or {theta.shape[0]}][{knot_t.shape[0]}]")
+        if seed is not None:
+            P, nsd = self.cfg.n_tangents, theta.shape[1] + sol.shape[0]
+            if seed.size != P * nsd:
+                raise ValueError(f"tangent_seed has {seed.size} values: expected [{P}][{nsd}]")
         self._check(self._lib.pbe_set_kinetics(
             self._h, law, theta.shape[1], theta.shape[0], _ptr(theta), sol_kind, sol.shape[0], _ptr(sol),
             knot_t.shape[0], _ptr(knot_t), _ptr(knot_T), per_sim, _ptr(seed)))
@@ -179,7 +203,15 @@ class Context:
         if not on_dev:
             n0 = _host(n0)
         rows = n0.shape[0] if n0.ndim == 2 else 1
-        stride = 0 if rows == 1 else self.cfg.n_bins * max(self.cfg.n_bins2, 1)
+        cells = self.cfg.n_bins * max(self.cfg.n_bins2, 1)
+        stride = 0 if rows == 1 else cells
+        S, P = self.n_sims, self.cfg.n_tangents
+        if on_dev:
+            _check_dev("n0", n0, self.device, [(cells,), (1, cells), (S, cells)])
+        elif n0.size not in (cells, S * cells):
+            raise ValueError(f"n0 has {n0.size} values: expected [1 or {S}][{cells}]")
+        _check_dev("n_final", n_final, self.device, [(S, cells)])
+        _check_dev("ndot_final", ndot_final, self.device, [(S, P, self.cfg.n_bins)])
         c0 = _host(np.atleast_1d(c0))
         ts = _host(t_samples) if t_samples is not None else np.zeros(1)
         tg = _host(target)
@@ -199,6 +231,8 @@ class Context:
             n0 = _host(n0)
         rows = n0.shape[0] if n0.ndim == 2 else 1
         stride = 0 if rows == 1 else self.cfg.n_bins
+        if on_dev:
+            _check_dev("n0", n0, self.device, [(self.cfg.n_bins,), (1, self.cfg.n_bins), (self.n_sims, self.cfg.n_bins)])
         c0 = _host(np.atleast_1d(c0)); ts = _host(t_samples); tg = _host(target)
         if stream is None:
             import torch

@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
             s_coef[slot].kap2 = 2.0 * sc.kap.v;
             s_coef[slot].beta2 = C > 0.0 ? (1.0 - 2.0 * C) : (C < 0.0 ? -(1.0 + 2.0 * C) : 0.0);
         }
-        if (pl >= 0 && pl < P) s_coef[slot].Cd[pl] = sc.C.d;
+        // every lane slot < P is written (unused lanes >= kp.P carry 0, never uninitialised smem)
+        if (lane < P) s_coef[slot].Cd[lane] = (pl >= 0) ? sc.C.d : 0.0;
         return true;
     };
     auto set_inactive = [&](int slot) {

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
         W.sign = sgn(W.G);
         W.active = kp.n_steps > 0 && kp.max_steps > 0;
         if (kp.max_steps <= 0) W.status = ST_MAXSTEPS;
-        W.depth = (int)min((long long)KB, kp.n_steps);
+        W.depth = (int)min(min((long long)KB, kp.n_steps), max(kp.max_steps, 1LL));   // never past max_steps
         W.sample = W.depth == kp.n_steps;
         if (lane == 0) s_sim[warp] = W;
     }
@@ -337,8 +337,11 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
                 W.G = growth(s, W.c, W.t);
                 if (q + 1 < d && sgn(W.G) != W.sign) { valid = q + 1; break; }   // sign change inside
             }
-            if (!fail && valid < d) {
-                // redo the valid prefix from the unchanged buffer (bitwise the same sub-steps)
+            if (valid < d) {
+                // redo the valid prefix from the unchanged buffer (bitwise the same sub-steps).  On a
+                // failure (NEG / INFEAS at sub-step valid - 1) the redo ends exactly at the failing step,
+                // which fails again there, so n_final holds the failing step's state like every other
+                // kernel (R-26) instead of the state after the whole block
                 W = W0;
                 W.depth = valid;
                 W.sample = W0.sample && false;
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
                 else if (W.nstep >= kp.max_steps) { W.status = ST_MAXSTEPS; W.active = 0; }
                 else {
                     W.sign = sgn(W.G);
-                    W.depth = (int)min((long long)KB, kp.n_steps - W.nstep);
+                    W.depth = (int)min(min((long long)KB, kp.n_steps - W.nstep), kp.max_steps - W.nstep);
                     W.sample = (W.nstep + W.depth == kp.n_steps);
                 }
                 if (!W.active && owner && lane == 0) sp.final_buf[s] = W.cur;

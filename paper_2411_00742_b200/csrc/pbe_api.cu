@@ -2,7 +2,8 @@
 //  pbe_api.cu — host side of libpbe: the C ABI declared in include/pbe.h.
 //  Validation, context-owned device memory, stream-ordered launches, kernel dispatch
 //  by (N, tangent lanes).  No computation of the method happens here: every step of
-//  the march runs in the CUDA kernels (k_resident.cuh, k_stream.cuh, k_cluster.cuh).
+//  the march runs in the CUDA kernels (k_resident.cuh incl. its cluster mode, k_stream.cuh,
+//  k_stream_tb.cuh, k_2d_fused.cuh, k_2d.cuh, k_adjoint.cuh).
 // =====================================================================================
 #include <cuda_runtime.h>
 
@@ -507,6 +508,7 @@ static pbe_status validate_run(pbe_ctx ctx, int32_t n_sims, const double* n0, in
     }
     if (ndot_final && P == 0) return fail(ctx, PBE_ERR_ARG, "ndot_final requires n_tangents > 0");
     (void)M;
+    (void)two_d;
     return PBE_OK;
 }
 
@@ -521,6 +523,9 @@ static pbe_status stage_run(pbe_ctx ctx, int32_t n_sims, const double* n0, int64
     const bool two_d = cf.n_bins2 > 0;
     const long long cells = (long long)N * (two_d ? cf.n_bins2 : 1);
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    // the ctx-owned input and output buffers are reused run after run: a run on another stream
+    // waits for the previous run's kernel (ev1) before they are overwritten
+    if (ctx->have_run && ctx->last_stream != st) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev1, 0));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->c0.p, c0, n_sims * sizeof(double), cudaMemcpyHostToDevice, st));
     if (!steps_mode)
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->tsamp.p, t_samples, M * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -539,6 +544,8 @@ static pbe_status stage_run(pbe_ctx ctx, int32_t n_sims, const double* n0, int64
     // unreached samples read as NaN (all-ones bytes)
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->rec.p, 0xff, (size_t)n_sims * M * (two_d ? 8 : 6) * sizeof(double), st));
     if (P) CUDA_TRY(ctx, cudaMemsetAsync(ctx->trec.p, 0xff, (size_t)n_sims * M * P * 5 * sizeof(double), st));
+    // loss reads NaN unless the kernel writes it (no target, 2D runs): never stale or uninitialised
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->loss.p, 0xff, (size_t)n_sims * sizeof(double), st));
     *n0_dev_out = n0_dev;
     return PBE_OK;
 }
@@ -707,6 +714,9 @@ pbe_status pbe_set_kinetics(pbe_ctx ctx, int32_t law, int32_t n_params, int32_t 
     else for (int p = 0; p < P && p < n_params; ++p) seed[(size_t)p * nsd + p] = 1.0;
 
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    // a previous run may still be reading theta / sol / knots / seed on its (non-blocking) stream:
+    // the synchronous copies below must not overwrite them under it
+    if (ctx->have_run) CUDA_TRY(ctx, cudaStreamSynchronize(ctx->last_stream));
     CUDA_TRY(ctx, ctx->theta.ensure(nth * sizeof(double)));
     CUDA_TRY(ctx, ctx->sol.ensure(3 * sizeof(double)));
     CUDA_TRY(ctx, ctx->knot_t.ensure(n_knots * sizeof(double)));
@@ -734,6 +744,7 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     const int N = cf.n_bins, P = cf.n_tangents;
     const bool two_d = cf.n_bins2 > 0;
     const bool steps_mode = cf.n_steps > 0;
+    if (two_d && target) return fail(ctx, PBE_ERR_ARG, "the 2D model has no RSS objective: target must be NULL");
 
     // kernel choice: register-resident when the simulation fits one CTA, else streaming
     int groups = 1;

@@ -30,6 +30,11 @@ from . import LAW_ARRHENIUS_GD, LAW_POLY, SOL_EXP, Context
 
 APPB_T = (10.0, 15.0, 20.0)
 APPB_S0 = (1.15, 1.25, 1.5)
+# c*(T) = 3.37 exp(0.036 T) at APPB_T (Eq. A.1, Table A.1 constants) as input data: the product
+# evaluates no kinetics on the host (workloads.APPB_CSAT holds the same numbers; a CPU test
+# re-derives them through the oracle)
+APPB_CSAT = (4.8303201270683465, 5.782943125562973, 6.923439919869901)
+SOL_DEFAULT = (3.37, 0.036)
 
 
 @dataclass
@@ -49,16 +54,20 @@ class Experiments:
 
 
 def make_experiments(N: int, n0: np.ndarray, t_max: float = 600.0, M: int = 600, dt_max: float = 0.05,
-                     truth=(8.86e6, 2.45e3, 3.7), sol=(3.37, 0.036), device: int = 0) -> Experiments:
+                     truth=(8.86e6, 2.45e3, 3.7), sol=SOL_DEFAULT, csat=None, device: int = 0) -> Experiments:
     """App. B in-silico campaign: c0 = S0 c*(T) for the 3 x 3 grid, targets (c, mu1/mu0)
-    sampled at M uniform times from the GPU FVM with the Arrhenius truth (R-28)."""
+    sampled at M uniform times from the GPU FVM with the Arrhenius truth (R-28).  csat: c*(T)
+    at the three temperatures APPB_T (input data; defaults to APPB_CSAT for the Table A.1
+    solubility, required for any other `sol`)."""
     import torch
     dL = 1200.0 / N
+    if csat is None:
+        if tuple(sol) != SOL_DEFAULT:
+            raise ValueError("make_experiments: pass csat = c*(T) at APPB_T for a non-default solubility")
+        csat = APPB_CSAT
     T = np.repeat(np.array(APPB_T), 3)
     S0 = np.tile(np.array(APPB_S0), 3)
-    # c*(T) for the initial concentrations is the solubility law (Eq. A.1) evaluated here, on
-    # the host, once per experiment (input preparation, not part of the march)
-    c0 = S0 * sol[0] * np.exp(sol[1] * T)
+    c0 = S0 * np.repeat(np.asarray(csat, dtype=np.float64), 3)
     t = np.linspace(t_max / M, t_max, M)
     ctx = Context(N, dL, dt_max=dt_max, n_samples=M, max_sims=9, device=device)
     ctx.set_kinetics(LAW_ARRHENIUS_GD, np.tile(np.array(truth), (9, 1)), SOL_EXP, np.array(sol),

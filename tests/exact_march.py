@@ -172,10 +172,12 @@ def march(num, *, N, dL, L_lo, limiter, courant, dt_fixed, dt_max, law, theta, s
 
 
 def march_2d(num, *, N1, N2, dL1, dL2, limiter, dt_fixed, law, theta, sol_kind, sol, T, f0, c0, rho_c, k_v,
-             t_samples):
-    """Exact 2D Godunov-split march (rows along L1, then columns along L2, flux form) with
-    fixed dt landing on the sample times; returns records (t, c, mu00, mu10, mu01, mu11,
-    mu02, mu12) and the final field [N2][N1]."""
+             t_samples, courant=None, dt_max=None, binding=None):
+    """Exact 2D Godunov-split march (rows along L1, then columns along L2, flux form) landing
+    on the sample times; returns records (t, c, mu00, mu10, mu01, mu11, mu02, mu12) and the
+    final field [N2][N1].  dt_fixed > 0: fixed dt; otherwise the SI's CFL rule (PAPER.md
+    L857-861) dt = nu min(dL1/|G1|, dL2/|G2|) (a zero rate does not limit), capped by dt_max.
+    `binding` (a list) receives, per CFL step, which dimension set dt (1, 2 or 0 = dt_max)."""
     f = [[num(f0[j * N1 + i]) for i in range(N1)] for j in range(N2)]
     c, t = num(c0), num(0)
     L1 = [(num(i) + num("0.5")) * num(dL1) for i in range(N1)]
@@ -191,9 +193,21 @@ def march_2d(num, *, N1, N2, dL1, dL2, limiter, dt_fixed, law, theta, sol_kind, 
         S = c / solubility(num, sol_kind, sol, Tn)
         G1 = growth(num, law, theta[:H], S, Tn)
         G2 = growth(num, law, theta[H:], S, Tn)
-        dt = num(dt_fixed)
+        if dt_fixed:
+            dt = num(dt_fixed)
+        else:
+            cand = []
+            if G1 != 0:
+                cand.append((num(courant) * num(dL1) / abs(G1), 1))
+            if G2 != 0:
+                cand.append((num(courant) * num(dL2) / abs(G2), 2))
+            if dt_max is not None:
+                cand.append((num(dt_max), 0))
+            dt, who = min(cand, key=lambda e: e[0]) if cand else (None, -1)   # None: unbounded
+            if binding is not None:
+                binding.append(who)
         tn = num(t_samples[m])
-        landing = t + dt >= tn - num("1e-9") * dt
+        landing = dt is None or t + dt >= tn - num("1e-9") * dt
         if landing:
             dt = tn - t
         C1, C2 = G1 * dt / num(dL1), G2 * dt / num(dL2)

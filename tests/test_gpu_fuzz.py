@@ -123,6 +123,9 @@ def random_case_2d(seed):
     return w
 
 
+DRAIN = 1e-4     # R-33: a moment below 1e-4 of its run maximum has lost > 99.99% of its mass
+
+
 @pytest.mark.parametrize("seed", range(max(12, NF // 4)))
 def test_fuzz_2d_matches_oracle(seed):
     import paper_2411_00742_b200 as pb
@@ -132,17 +135,22 @@ def test_fuzz_2d_matches_oracle(seed):
     assert np.array_equal(g["status"], o["status"]) and np.array_equal(g["steps"], o["steps"]), (g["status"], o["status"])
     a, b = g["samples"], o["samples"]
     assert np.array_equal(np.isnan(a), np.isnan(b))
-    # relative to each moment's largest value over the run: a moment that the outflow drove down by
-    # ten orders of magnitude is the remainder of a cancellation (its own relative error is not a
-    # property of either implementation)
-    scale = np.nanmax(np.abs(b), axis=1, keepdims=True)
+    # element-wise 1e-10 relative (north star), except for a moment the outflow boundary has drained
+    # below DRAIN of its largest value over the run: its absolute error is the rounding of the
+    # fluxes that carried that mass out, so it is compared at 1e-10 of its run maximum (reading
+    # R-33)
+    runmax = np.nanmax(np.abs(b), axis=1, keepdims=True)
+    drained = np.abs(b) < DRAIN * runmax
+    scale = np.where(drained, runmax, np.abs(b))
     ok = ~np.isnan(b)
     if ok.any():
         assert np.max((np.abs(a - b) / np.maximum(scale, 1e-300))[ok]) <= 1e-10
     for s in range(w.n_sims):
         if o["status"][s] == 0:
             f = o["f_final"][s].reshape(-1)
-            sc = max(np.max(np.abs(f)), np.max(np.abs(w.n0)))   # same conditioning argument as above
+            sc = np.max(np.abs(f))
+            if sc < DRAIN * np.max(np.abs(w.n0)):            # the whole field drained (R-33)
+                sc = np.max(np.abs(w.n0))
             assert np.max(np.abs(g["n_final"][s] - f)) <= 1e-9 * sc
 
 

@@ -82,6 +82,28 @@ def test_pin1_kinetics_vs_50_digits(T):
     assert G == pytest.approx(float(G_ref), rel=2e-14)
 
 
+# R-12 dissolution constants deliberately different from the growth constants, so a branch that
+# reads theta[0..2] instead of theta[3..5] (or mixes them) is caught
+ARRH_DISTINCT = (8.86e6, 2.45e3, 3.7, 2.0e5, 2.0e3, 1.5)
+
+
+@pytest.mark.parametrize("T", [10.0, 25.0])
+@pytest.mark.parametrize("c", [8.0, 4.0, 5.5])
+def test_pin1_dissolution_branch_own_parameters_vs_50_digits(T, c):
+    # Eq. A.2 for S > 1 with (kg, Eg, g) = theta[0..2]; R-12 for S < 1 with (kd, Ed, d) = theta[3..5]
+    w = _w_exp(T=T, theta=ARRH_DISTINCT)
+    Tk, cs, S, G = oracle.kinetics(w, ARRH_DISTINCT, 0.0, c)
+    cs_ref = mp.mpf("3.37") * mp.exp(mp.mpf("0.036") * T)
+    S_ref = c / cs_ref
+    k = [mp.mpf(repr(x)) for x in ARRH_DISTINCT]
+    if S_ref > 1:
+        G_ref = k[0] * mp.exp(-k[1] / (T + mp.mpf("273.15"))) * (S_ref - 1) ** k[2]
+    else:
+        G_ref = -(k[3] * mp.exp(-k[4] / (T + mp.mpf("273.15"))) * (1 - S_ref) ** k[5])
+    assert (S > 1) == (S_ref > 1)
+    assert G == pytest.approx(float(G_ref), rel=2e-14)
+
+
 def test_pin1_base_case_growth_value():
     # Table 1 base case: T = 15 C, c0 = 8 -> S0 = 1.38338, G(S0) = 51.79 um/min
     T, cs, S, G = oracle.kinetics(_w_exp(), W.ARRHENIUS_DEFAULT, 0.0, 8.0)
@@ -124,6 +146,9 @@ def test_workload_constants_rederived_through_oracle():
         assert oracle.kinetics(_w_exp(T=T), W.ARRHENIUS_DEFAULT, 0.0, 1.0)[1] == pytest.approx(cs, rel=1e-15)
     w2 = _small(sol=np.array(W.SOL_POLY_DEFAULT))
     assert oracle.kinetics(w2, [0.5], 0.0, 1.0)[1] == pytest.approx(W.C2_C0, rel=1e-15)
+    # the estimation driver's copy of the same table (product code evaluates no kinetics)
+    from paper_2411_00742_b200 import estimate as E
+    assert E.APPB_CSAT == W.APPB_CSAT and E.APPB_T == W.APPB_T and E.SOL_DEFAULT == W.SOL_EXP_DEFAULT
 
 
 # ------------------------------------------------------------------------------------
@@ -269,13 +294,14 @@ def test_pin9_poly_kinetics_cfl_coupled_exact(lim):
     _compare_exact(w, X.Num("fraction"), 1e-13)
 
 
+@pytest.mark.parametrize("theta", [W.ARRHENIUS_DEFAULT, ARRH_DISTINCT])
 @pytest.mark.parametrize("c0", [8.0, 4.0])
-def test_pin9_arrhenius_growth_dissolution_50_digits(c0):
+def test_pin9_arrhenius_growth_dissolution_50_digits(c0, theta):
     # exp-based kinetics (Eq. A.2 + R-12 dissolution), exponential solubility, dt_max cap,
     # time-varying T: brute force at 50 digits.  c0 = 4 < c*(15) -> dissolution.
     rng = np.random.default_rng(5)
     n0 = _int_seed(rng, 10) * 1e3
-    w = _small(law=W.LAW_ARRHENIUS, theta=np.array([W.ARRHENIUS_DEFAULT]), sol_kind=W.SOL_EXP,
+    w = _small(law=W.LAW_ARRHENIUS, theta=np.array([theta]), sol_kind=W.SOL_EXP,
                sol=np.array(W.SOL_EXP_DEFAULT), knot_t=np.array([0.0, 0.1]), knot_T=np.array([[15.0, 25.0]]),
                n0=n0[None, :], c0=np.array([c0]), dL=10.0, dt_max=0.02,
                t_samples=np.array([0.05, 0.1]))
@@ -538,3 +564,22 @@ def test_status_infeasible_and_maxsteps():
     w = W.c1_growth(); w.max_steps = 10
     r = oracle.run(w)
     assert r["status"][0] == 5 and r["steps"][0] == 10
+
+
+def test_appb_targets_are_the_method_of_moments():
+    # workloads/data/appb_targets.npy (tools/gen_appb_targets.py): spot-check experiment 4
+    # (T = 15 C, S0 = 1.25) over its first 5 samples with an independent RK4 run at h = 0.01
+    from tests import mom
+    N = 2000
+    dL = 1200.0 / N
+    n0 = W.gaussian_seed(N, dL, m0=1.0)
+    L = W.bin_centers(N, dL)
+    y = np.array([W.APPB_S0[1] * W.APPB_CSAT[1]] + [np.sum(dL * L ** k * n0) for k in range(4)])
+    w = W.Workload(name="appb", N=N, dL=dL, law=W.LAW_ARRHENIUS, theta=np.array([W.ARRHENIUS_DEFAULT[:3]]),
+                   sol_kind=W.SOL_EXP, sol=np.array(W.SOL_EXP_DEFAULT), knot_t=np.array([0.0]),
+                   knot_T=np.array([[15.0]]), n0=n0[None, :], c0=y[:1].copy())
+    tg = W.appb_target(np.array([4]), np.arange(1.0, 6.0), y[:1])[0]
+    for m in range(5):
+        w.c0 = np.array([y[0]])
+        y = mom.solve(w, y[1:], 1.0, 100)
+        assert tg[m, 0] == pytest.approx(y[0], rel=1e-9) and tg[m, 1] == pytest.approx(y[2] / y[1], rel=1e-9)

@@ -59,6 +59,34 @@ def test_2d_march_matches_exact_rational_brute_force(lim):
     assert np.max(np.abs(r["f_final"][0] - fe)) <= 1e-13 * np.max(fe)
 
 
+@pytest.mark.parametrize("lim", [0, 1])
+def test_2d_cfl_rule_matches_exact_rational_brute_force(lim):
+    # SI L857-861: dt = nu min(dL1/|G1|, dL2/|G2|).  dL1 = 1 != dL2 = 0.5 and G2 = (S-1)^2 vs
+    # G1 = S-1, with a mass coupling strong enough that the binding dimension switches from L2
+    # to L1 as S falls: a dt taken from one dimension only, or with the wrong bin width,
+    # changes every record.
+    rng = np.random.default_rng(9)
+    N1, N2 = 6, 5
+    f0 = np.array([float(x) for x in rng.integers(0, 20, N1 * N2)]) * 0.5
+    kw = dict(theta=[1.0, 0.0, 0.0, 1.0], sol=[2.0, 0.0, 0.0], rho_c=0.1, k_v=0.5, t_samples=[1.0, 2.0])
+    w = W.Workload(name="t2cfl", N=N1, dL=1.0, N2=N2, dL2=0.5, dt_fixed=0.0, law=W.LAW_POLY,
+                   theta=np.array([kw["theta"]]), sol_kind=W.SOL_POLY, sol=np.array(kw["sol"]),
+                   knot_t=np.array([0.0]), knot_T=np.array([[15.0]]), n0=f0[None, :], c0=np.array([4.0]),
+                   rho_c=kw["rho_c"], k_v=kw["k_v"], t_samples=np.array(kw["t_samples"]), limiter=lim,
+                   courant=0.9)
+    r = oracle.run2d(w)
+    binding = []
+    recs, f = X.march_2d(X.Num("fraction"), N1=N1, N2=N2, dL1=1.0, dL2=0.5, limiter=lim, dt_fixed=0,
+                         law=W.LAW_POLY, sol_kind=1, T=15.0, f0=list(f0), c0=4.0, courant=0.9,
+                         binding=binding, **kw)
+    assert 1 in binding and 2 in binding, binding          # both dimensions limit dt at some step
+    assert r["status"][0] == 0 and r["steps"][0] == len(binding)
+    ex = np.array([[float(v) for v in rec] for rec in recs])
+    assert np.allclose(r["samples"][0], ex, rtol=1e-13, atol=0)
+    fe = np.array([[float(v) for v in row] for row in f])
+    assert np.max(np.abs(r["f_final"][0] - fe)) <= 1e-13 * np.max(fe)
+
+
 def test_2d_conservation_and_positivity():
     w = W.c2d_base(120, 60, t_max=20.0, M=20)
     r = oracle.run2d(w)

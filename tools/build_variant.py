@@ -16,6 +16,6 @@ if r.returncode:
     sys.exit(r.stderr[-3000:])
 lines = r.stdout.splitlines() + r.stderr.splitlines()
 for k, l in enumerate(lines):
-    if "Compiling entry function" in l and any(x in l for x in sys.argv[-1:]) is not None and "k_2d_fused" in l:
+    if "Compiling entry function" in l and "k_2d_fused" in l:
         print(tag, lines[k + 2].strip(), "|", lines[k + 3].strip())
 print(out)

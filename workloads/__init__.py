@@ -6,7 +6,7 @@ mass balance.  It only builds arrays (seed distributions, parameter draws, sampl
 times, temperature knots) with the shapes of the paper's workloads (DESIGN.md
 "Input recipe"), and hard-coded constants where an input value would otherwise need
 the method's arithmetic (each such constant is re-derived by a test through the
-oracle, tests/test_workloads.py).
+oracle, tests/test_oracle_pins.py::test_workload_constants_rederived_through_oracle).
 
 Paper sources for the shapes: Table 1 (Gaussian seed, mean 400 um,
 sigma 30 um, m0 = 1 g/kg, c0 = 8 g/kg, T = 15 C, L_max = 1200 um, rho_c, k_v);
@@ -17,6 +17,7 @@ experiments, T in {10,15,20} C x S0 in {1.15,1.25,1.5}, 600 samples); eq-poly_gr
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field, replace
 from typing import Optional
 
@@ -38,7 +39,8 @@ SOL_EXP_DEFAULT = (3.37, 0.036)
 SOL_POLY_DEFAULT = (3.37, 3.37 * 0.036, 3.37 * 0.036 * 0.036 / 2.0)
 
 # c*(T) values needed as INPUTS (initial concentrations).  Hard-coded so this module
-# holds no kinetics; tests/test_workloads.py re-derives each through the oracle.
+# holds no kinetics; tests/test_oracle_pins.py::test_workload_constants_rederived_through_oracle
+# re-derives each through the oracle.
 #   C2: c0 = c*_poly(15) = 3.37 + 0.12132*15 + 0.00218376*225
 C2_C0 = 5.681146
 #   C5 / App. B: c0 = S0 * 3.37 exp(0.036 T) for T in (10, 15, 20), S0 in (1.15, 1.25, 1.5)
@@ -150,6 +152,23 @@ def _target(c0: np.ndarray, t: np.ndarray, L0: float = 400.0) -> np.ndarray:
     return out
 
 
+_APPB = None
+
+
+def appb_target(e: np.ndarray, t: np.ndarray, c0: np.ndarray) -> np.ndarray:
+    """App. B "measurements" for experiments e (0..8) at sample times t: (c, mu1/mu0) of the
+    1D method of moments with the Arrhenius truth, precomputed at
+    t = 1, 2, ..., 600 min by tools/gen_appb_targets.py (workloads/data/appb_targets.npy).
+    Sample grids that are not a subset of that grid fall back to the closed-form _target."""
+    global _APPB
+    if _APPB is None:
+        _APPB = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "appb_targets.npy"))
+    idx = np.rint(t).astype(np.int64) - 1
+    if not (np.all(np.abs(t - (idx + 1)) == 0.0) and idx.min() >= 0 and idx.max() < _APPB.shape[1]):
+        return _target(c0, t)
+    return _APPB[np.asarray(e)][:, idx, :].copy()
+
+
 # ------------------------------------------------------------------------------------
 # BASELINE.json configs
 # ------------------------------------------------------------------------------------
@@ -233,7 +252,7 @@ def c5_ensemble(n_sims: int = 4096, N: int = 2000, t_max: float = 600.0, M: int 
         law=LAW_POLY, theta=theta, sol_kind=SOL_EXP, sol=np.array(SOL_EXP_DEFAULT),
         knot_t=np.array([0.0]), knot_T=T[:, None].copy(),
         n0=gaussian_seed(N, dL, m0=1.0)[None, :], c0=c0, t_samples=t,
-        target=_target(c0, t), n_tangents=n_tangents)
+        target=appb_target(e, t, c0), n_tangents=n_tangents)
 
 
 def next3_estimation(n_params: int = 1000, N: int = 2000, t_max: float = 600.0, M: int = 600,
@@ -257,7 +276,7 @@ def next3_estimation(n_params: int = 1000, N: int = 2000, t_max: float = 600.0, 
         name=f"next3_estimation_P{n_params}_N{N}", N=N, dL=dL, dt_max=dt_max, max_steps=int(1.2 * t_max / dt_max) + 1000,
         law=LAW_POLY, theta=theta, sol_kind=SOL_EXP, sol=np.array(SOL_EXP_DEFAULT),
         knot_t=np.array([0.0]), knot_T=T[:, None].copy(),
-        n0=gaussian_seed(N, dL, m0=1.0)[None, :], c0=c0, t_samples=t, target=_target(c0, t))
+        n0=gaussian_seed(N, dL, m0=1.0)[None, :], c0=c0, t_samples=t, target=appb_target(e, t, c0))
 
 
 CONFIGS = {

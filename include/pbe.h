@@ -207,6 +207,7 @@ typedef struct {
                                 (measured on the launch stream; valid after pbe_moments) */
     int32_t steps_per_pass;  /* time steps fused per HBM pass (k_stream temporal blocking, NEXT-4;
                                 1 otherwise) */
+    int32_t warp_specialized;/* 1: k_resident_ws (primal warps + tangent warps), 0 otherwise */
 } pbe_run_info;
 pbe_status pbe_last_run_info(pbe_ctx ctx, pbe_run_info* info);
 

@@ -53,7 +53,7 @@ class _Config(C.Structure):
 class RunInfo(C.Structure):
     _fields_ = [("kernel", C.c_int32), ("launches", C.c_int32), ("threads_per_cta", C.c_int32),
                 ("ctas", C.c_int32), ("cluster", C.c_int32), ("bins_per_thread", C.c_int32),
-                ("main_ms", C.c_double), ("steps_per_pass", C.c_int32)]
+                ("main_ms", C.c_double), ("steps_per_pass", C.c_int32), ("warp_specialized", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

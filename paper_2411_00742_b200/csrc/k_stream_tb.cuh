@@ -376,7 +376,9 @@ __global__ void __launch_bounds__(TB_NT, PBE_TB_MINB) k_stream_tb(const StreamTB
             kp.status[s] = W.status;
             kp.steps[s] = W.nstep;
             if (kp.loss) kp.loss[s] = __longlong_as_double(0x7ff8000000000000ll);
-            if (W.nstep == 0) sp.final_buf[s] = 0;
+            // never marched (inactive from the start): n_final = n0.  A failure in the very first
+            // step also has nstep = 0 but its buffer was set to the failing step's state (R-26)
+            if (W.nstep == 0 && W.status != ST_NEG && W.status != ST_INFEAS) sp.final_buf[s] = 0;
         }
     }
 }

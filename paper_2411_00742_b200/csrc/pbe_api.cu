@@ -18,6 +18,7 @@
 #include "../../include/pbe.h"
 #include "pbe_device.cuh"
 #include "k_resident.cuh"
+#include "k_resident_ws.cuh"
 #include "k_stream.cuh"
 #include "k_2d.cuh"
 #include "k_2d_fused.cuh"
@@ -75,6 +76,8 @@ struct pbe_ctx_s {
     int group_max = 8;       // max tangent lanes per resident CTA (env PBE_LANES_PER_CTA)
     bool cluster2 = false;   // env PBE_CLUSTER2: 2-CTA clusters at 2 CTAs/SM for small N
     int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
+    bool ws = true;          // env PBE_WS=0: lockstep k_resident instead of k_resident_ws for P >= 1
+    int ws_variant = 0;      // env PBE_WS_VARIANT: k_resident_ws tuning variant (A/B only)
     bool temporal_block = true;  // NEXT-4 temporal blocking for uncapped-CFL steps mode in
                                  // k_stream (1.27x plain streaming on 64 x 1e6); env
                                  // PBE_TEMPORAL_BLOCK=0 selects plain streaming
@@ -116,6 +119,26 @@ size_t resident_smem(const ResidentVariant& v, int nt) {
     return (size_t)2 * 4 * (1 + v.P) * (nt + 2) * sizeof(double)      // halo, 2 parities
            + (size_t)v.K * nt * sizeof(double);                        // mu3 weights [K][NT]
 }
+
+// k_resident_ws<P, K, NT>: scalar chain off the critical path (a scalar warp runs the next step's
+// kinetics while NT - 32 bin threads sweep the tangent lanes), P >= 1 lanes
+struct WsVariant {
+    int P, K, nt;
+    KernelFn fn;
+    bool xs;
+    int tag;              // A/B tuning variant (PBE_WS_VARIANT); 0 = default
+    int bins() const { return (nt - 32) * K; }
+    size_t smem() const { return pbe::ws_smem_doubles(P, K, nt - 32, xs) * sizeof(double); }
+};
+#define WV(P, K, T) WsVariant{P, K, T, &pbe::k_resident_ws<P, K, T, false, false, 0>, false, 0}
+#define WVX(P, K, T, XS, HALF, LAG, TAG) WsVariant{P, K, T, &pbe::k_resident_ws<P, K, T, XS, HALF, LAG>, XS, TAG}
+const WsVariant kResidentWS[] = {
+    WV(8, 9, 64), WV(8, 9, 128), WV(8, 9, 256),
+    WVX(8, 9, 256, true, false, 2, 1), WVX(8, 9, 256, true, true, 2, 2), WVX(8, 9, 256, true, false, 0, 3),
+    WVX(8, 9, 256, true, true, 0, 4), WVX(8, 9, 256, false, true, 2, 5), WVX(8, 9, 256, false, false, 2, 6),
+};
+#undef WVX
+#undef WV
 
 #define RV(P, K, T) ResidentVariant{P, K, T, &pbe::k_resident<P, K, T>}
 const ResidentVariant kResident[] = {
@@ -209,6 +232,19 @@ const ResidentVariant* pick_resident(int N, int P, int group_max, int* groups, i
                                       (abs(v.K - k_pref) == abs(best->K - k_pref) && v.K < best->K))
                                    : v.K < best->K;
         if (closer) best = &v;
+    }
+    return best;
+}
+
+// scalar-chain-overlapped variant for P tangent lanes (lanes_per_cta(P) exactly: no idle lane
+// padding) and N bins: the fewest threads that cover N
+const WsVariant* pick_ws(int N, int P, int tag) {
+    const WsVariant* best = nullptr;
+    for (const auto& v : kResidentWS) {
+        if (v.tag != tag) continue;
+        if (v.P != lanes_per_cta(P, 8) || v.bins() < N) continue;
+        if (v.smem() + static_smem(v.fn) > 227 * 1024) continue;
+        if (!best || v.nt < best->nt) best = &v;
     }
     return best;
 }
@@ -593,6 +629,9 @@ const char* pbe_version(void) { return "libpbe 0.1 (sm_100a)"; }
 int pbe_debug_phase_cycles(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, pbe::g_phase_cycles, sizeof(pbe::g_phase_cycles)) == cudaSuccess ? 0 : 1;
 }
+int pbe_debug_ws_cycles(unsigned long long* out) {       // [8], see k_resident_ws.cuh
+    return cudaMemcpyFromSymbol(out, pbe::g_ws_cycles, sizeof(pbe::g_ws_cycles)) == cudaSuccess ? 0 : 1;
+}
 int pbe_debug_stream_cycles(unsigned long long* out) {    // [1024][5], see k_stream.cuh
     return cudaMemcpyFromSymbol(out, pbe::g_stream_cycles, sizeof(pbe::g_stream_cycles)) == cudaSuccess ? 0 : 1;
 }
@@ -644,6 +683,8 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (const char* e = getenv("PBE_LANES_PER_CTA")) ctx->group_max = atoi(e);
     if (const char* e = getenv("PBE_CLUSTER2")) ctx->cluster2 = atoi(e) != 0;
     if (const char* e = getenv("PBE_RESIDENT_K")) ctx->resident_k = atoi(e);
+    if (const char* e = getenv("PBE_WS")) ctx->ws = atoi(e) != 0;
+    if (const char* e = getenv("PBE_WS_VARIANT")) ctx->ws_variant = atoi(e);
     if (const char* e = getenv("PBE_TEMPORAL_BLOCK")) ctx->temporal_block = atoi(e) != 0;
     if (const char* e = getenv("PBE_2D_UNFUSED")) ctx->unfused_2d = atoi(e) != 0;
     ctx->device = device;
@@ -773,7 +814,11 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
     if (kind == PBE_KERNEL_CLUSTER && !cv)
         return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit a 16-CTA cluster", N, P);
     if (two_d) kind = PBE_KERNEL_2D;
-    if (kind == PBE_KERNEL_RESIDENT && !rv)
+    // P >= 1 lanes in one CTA: the warp-specialised resident kernel (primal and tangent warps
+    // overlap the per-step scalar chain with the sweep); lane groups (PBE_LANES_PER_CTA) keep k_resident
+    const WsVariant* ws = (kind == PBE_KERNEL_RESIDENT && P >= 1 && ctx->ws && groups == 1 && !two_d)
+                              ? pick_ws(N, P, ctx->ws_variant) : nullptr;
+    if (kind == PBE_KERNEL_RESIDENT && !rv && !ws)
         return fail(ctx, PBE_ERR_ARG, "N = %d with %d tangent lanes does not fit the resident kernel", N, P);
     if (kind == PBE_KERNEL_STREAM && !sv)
         return fail(ctx, PBE_ERR_ARG, "the streaming kernel supports at most 4 tangent lanes (got %d)", P);
@@ -792,6 +837,22 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
         pbe_status r = ctx->unfused_2d ? launch_2d(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st)
                                        : launch_2d_fused(ctx, kp, n_sims, n0_dev, n0_stride, n_final, st);
         if (r != PBE_OK) return r;
+    } else if (kind == PBE_KERNEL_RESIDENT && ws) {
+        const int nt = ws->nt;
+        const size_t smem = ws->smem();
+        CUDA_TRY(ctx, cudaFuncSetAttribute(ws->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kp.G = 1;
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+        ws->fn<<<n_sims, nt, smem, st>>>(kp);
+        CUDA_TRY(ctx, cudaGetLastError());
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+        ctx->info.kernel = PBE_KERNEL_RESIDENT;
+        ctx->info.launches = 1;
+        ctx->info.threads_per_cta = nt;
+        ctx->info.ctas = n_sims;
+        ctx->info.cluster = 1;
+        ctx->info.bins_per_thread = ws->K;
+        ctx->info.warp_specialized = 1;
     } else if (kind == PBE_KERNEL_RESIDENT) {
         const int nt = ((N + rv->K - 1) / rv->K + 31) / 32 * 32;
         const size_t smem = resident_smem(*rv, nt);

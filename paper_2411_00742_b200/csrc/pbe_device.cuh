@@ -325,6 +325,20 @@ __device__ __forceinline__ void psi_half_d(double a, double b, double& h, double
     qb = ar * ar;
 }
 
+// The same three values without a branch around the reciprocal (the divisor is replaced by 1
+// on inactive faces and the result selected afterwards): bitwise identical to psi_half_d, but
+// the faces of a sweep stay in one basic block, so their reciprocal chains can overlap.
+__device__ __forceinline__ void psi_half_d_bf(double a, double b, double& h, double& qa, double& qb) {
+    const double ab = a * b;
+    const bool act = ab > 0.0;
+    const double r0 = rcp_nr(act ? a + b : 1.0);
+    const double r = act ? r0 : 0.0;
+    const double br = b * r, ar = a * r;
+    h = ab * r;
+    qa = br * br;
+    qb = ar * ar;
+}
+
 // Select-free van Leer half slope (primal paths): h = ab/(a+b) for ab > 0, else exactly 0,
 // as (a|b| + |a|b) / (2 (|a| + |b|)).  The two products are rounded separately (no FMA
 // contraction), so for ab < 0 they cancel exactly and for ab > 0 the numerator is 2 round(ab);

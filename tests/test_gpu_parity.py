@@ -409,11 +409,12 @@ def test_temporal_blocking_max_steps_and_failure(temporal_blocking):
     g, o = _check(w, kernel=pb.KERNEL_STREAM)
     assert g["info"]["steps_per_pass"] == 8
     assert np.all(g["status"] == 5) and np.all(g["steps"] == 13)
-    # crystal mass 5000x the seed mass: the first step drives c below 0 (INFEASIBLE at step 1)
+    # crystal mass 5000x the seed mass: the first step drives c below 0 (INFEASIBLE in step 1,
+    # which is not counted: steps = completed steps)
     wf = W.c4_sweep(4000, batch=2, n_steps=40)
     wf.rho_c = 1.11e-12 * 5000.0
     g, o = _check(wf, kernel=pb.KERNEL_STREAM)
-    assert np.all(g["status"] == 4) and np.all(g["steps"] == 1)
+    assert np.all(g["status"] == 4) and np.all(g["steps"] == 0)
     r = _gpu(wf, kernel=pb.KERNEL_RESIDENT)             # same semantics in the resident kernel
     assert np.array_equal(r["status"], g["status"]) and np.array_equal(r["steps"], g["steps"])
     assert np.max(np.abs(r["n_final"] - g["n_final"])) <= RTOL_N * np.max(np.abs(r["n_final"]))
@@ -432,3 +433,60 @@ def test_outflow_boundary_all_kernels(kernel, N, P, steps_mode, monkeypatch):
     w = W.replace(w, n0=W.gaussian_seed(N, 1200.0 / N, mean=1120.0, sigma=50.0)[None, :])
     g, o = _check(w, mode=oracle.MODE_DUAL if P else oracle.MODE_DOUBLE, kernel=kernel)
     assert g["info"]["kernel"] == kernel
+
+
+# ---------------------------------------------------------------------------------------
+# k_resident_ws (scalar chain overlapped with the tangent sweep) and the lockstep k_resident
+# ---------------------------------------------------------------------------------------
+@pytest.fixture(params=["ws", "lockstep"])
+def resident_kind(request, monkeypatch):
+    monkeypatch.setenv("PBE_WS", "1" if request.param == "ws" else "0")   # read by pbe_create
+    return request.param
+
+
+def _expect_kind(g, kind):
+    assert g["info"]["kernel"] == 1 and g["info"]["warp_specialized"] == (1 if kind == "ws" else 0)
+
+
+def test_resident_kinds_cycling_sign_changes(resident_kind):
+    """C3-shaped temperature cycling with 8 tangent lanes: G changes sign with T, so the march
+    alternates between the two sweep directions (separate step loops in k_resident_ws)."""
+    w = W.c3_cycling(N=600, t_max=240.0, M=24, dt_max=0.05)
+    w = W.replace(w, n_tangents=6, n0=W.gaussian_seed(600, 2.0, mean=300.0, sigma=40.0)[None, :])
+    g, o = _check(w, mode=oracle.MODE_DUAL)
+    _expect_kind(g, resident_kind)
+    s = o["samples"][0]
+    assert np.any(np.diff(s[:, 1]) > 0) and np.any(np.diff(s[:, 1]) < 0)   # growth and dissolution
+
+
+def test_resident_kinds_c5_loss_gradient(resident_kind):
+    w = W.c5_ensemble(n_sims=12, N=900, t_max=30.0, M=30)
+    g, o = _check(w, mode=oracle.MODE_DUAL)
+    _expect_kind(g, resident_kind)
+    lo, go = oracle.loss_and_grad(o["samples"], o["tsamples"], w.target)
+    assert np.allclose(g["loss"], lo, rtol=1e-9, atol=0)
+    assert np.allclose(g["grad"], go, rtol=1e-8, atol=1e-9 * np.max(np.abs(go)))
+
+
+def test_resident_kinds_failure_with_tangents(resident_kind):
+    """INFEASIBLE part-way through a tangent run: earlier records valid, later ones NaN (R-26),
+    loss and gradient NaN, the other simulations unaffected."""
+    w = W.c5_ensemble(n_sims=3, N=400, t_max=20.0, M=20)
+    # constant G = 3 um/min regardless of S: the crystal mass grows until sim 1 (c0 = 0.05 g/kg)
+    # runs out of solute; 8 lanes seeded over (G, a, b) so every lane is non-trivial
+    seed = np.random.default_rng(5).standard_normal((8, 3))
+    w = W.replace(w, law=W.LAW_CONST, theta=np.full((3, 1), 3.0), c0=np.array([w.c0[0], 0.05, w.c0[2]]),
+                  tangent_seed=seed)
+    g, o = _check(w, mode=oracle.MODE_DUAL)
+    _expect_kind(g, resident_kind)
+    assert g["status"][1] == 4 and g["status"][0] == 0 and g["status"][2] == 0
+    assert np.isnan(g["loss"][1]) and np.all(np.isnan(g["grad"][1])) and np.all(np.isfinite(g["grad"][0]))
+
+
+def test_resident_kinds_steps_mode_and_lane_counts(resident_kind):
+    """Steps mode with capped steps (tangents do not vanish) and 5 lanes of an 8-lane kernel."""
+    w = W.c5_ensemble(n_sims=2, N=500, t_max=10.0, M=10, n_tangents=5)
+    w = W.replace(w, n_steps=77, t_samples=np.array([1.0]), target=None)
+    g, o = _check(w, mode=oracle.MODE_DUAL)
+    _expect_kind(g, resident_kind)
+    assert np.all(g["steps"] == 77) and np.any(g["ndot_final"] != 0.0)

@@ -1,14 +1,15 @@
 #!/usr/bin/env python
 """Benchmark of the batched PBE finite-volume march (BASELINE.json metric: bin-updates/s).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c4|c3|c2|c1]
-                  [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c4|c3|c2|c1|c2d]
+                  [--scaling strong|weak] [--impl ours|reference] [--quick]
 
 A bench "step" is one pass of the whole hot path (rows a1-a8: the complete time-march of
 every simulation of this rank's batch, one pbe_run_batch) over one batch of synthetic
-input.  Default workload = BASELINE config 5 (the one the metric is quoted on at
-1/2/4/8 GPUs): 4096 kinetic parameter sets PER GPU (weak scaling: the global ensemble is
-4096 N sims, sharded round-robin), 2000 bins, 8 forward-mode tangent lanes, 600 samples.
+input.  Default workload = BASELINE config 5 as written (the one the metric is quoted on at
+1/2/4/8 GPUs): 4096 kinetic parameter sets in total, sharded round-robin over the GPUs
+(strong scaling; --scaling weak keeps 4096 per GPU), 2000 bins, 8 forward-mode tangent
+lanes, 600 samples.
 
 One JSON line on rank 0 (see DESIGN.md "Measurement" for every field's definition):
   value      bin-updates/s over all ranks, inputs resident in HBM, CUDA events on the
@@ -16,8 +17,9 @@ One JSON line on rank 0 (see DESIGN.md "Measurement" for every field's definitio
   e2e        the same metric through the C ABI with pinned HOST buffers: the H2D copy of
              each step's inputs and the D2H read of its records (moments, status, steps,
              loss, gradient) inside the timed region
-  roofline   the dominant kernel (k_resident: the only kernel of the step) against the FP64
-             FMA peak (bound "alu"), or HBM for the streaming workload (bound "hbm")
+  roofline   the dominant kernel (k_resident_ws: the only kernel of the step): FP64 instructions
+             of the method per bin-update x rate against the DFMA throughput measured in the
+             same run (bound "alu"), or HBM for the streaming workloads (bound "hbm")
   cpu_baseline   the CPU oracle timed on a bounded sample on this host's cores
   --impl reference   the CPU oracle as the reference arm (the paper ships no code)
 """
@@ -49,10 +51,13 @@ UNIT = "bin-updates/s"
 def make_workload(name: str, world: int, args):
     """The GLOBAL workload (all ranks) and a short description for config."""
     if name == "c5":
-        w = W.c5_ensemble(n_sims=4096 * world)
-        desc = dict(workload="C5 ensemble + forward-mode tangents", sims_per_gpu=4096, global_sims=4096 * world,
-                    bins=2000, tangent_lanes=8, samples=600, t_max_min=600.0, dt_max=0.05, law="polynomial k=8",
-                    limiter="van Leer")
+        strong = args.scaling == "strong"
+        S = 4096 if strong else 4096 * world
+        w = W.c5_ensemble(n_sims=S)
+        desc = dict(workload="C5 ensemble + forward-mode tangents", global_sims=S,
+                    sims_per_gpu=S // world if strong else 4096, bins=2000, tangent_lanes=8, samples=600,
+                    t_max_min=600.0, dt_max=0.05, law="polynomial k=8", limiter="van Leer",
+                    target="App. B method-of-moments traces (workloads/data/appb_targets.npy)")
     elif name == "c4":
         N = args.bins or 1_000_000
         b = args.batch or 64
@@ -88,16 +93,21 @@ def replicate_single(w, world: int):
     return w.subset(np.zeros(world, dtype=np.int64)) if w.n_sims == 1 else w
 
 
-# FP64 flops per bin-update of the method: FMA = 2, div = 1.
-def flops_per_bin_update(limiter: int, P: int) -> float:
+# FP64 INSTRUCTIONS per bin-update of the method in the flux form the kernels implement
+# (DESIGN.md §5 "Roofline"; each DFMA / DMUL / DADD is one instruction on the FP64 pipe, the
+# reciprocal's MUFU seed runs on the XU pipe):
+#   van Leer primal 15: a, b (2), ab (1), a + b (1), Newton reciprocal (4), h = ab r (1),
+#       F = C n_up + kappa psi (2), update (2), mu3 (1), clip test (1)
+#   tangent support per face 10: b r, a r (2), qa, qb (2), kappa qa, kappa qb (2),
+#       g = n_up + beta psi (1), dg (1), w_mid (2)
+#   per tangent lane 7: lane flux (3), update (2), Cdot dg (1), mu3dot (1)
+#   upwind: primal 6 (F 1, update 2, mu3 1, clip 1, n_up 1), lane 5 (flux 1, update 2, Cdot 1, mu3dot 1)
+# SURVEY §8(d) estimated ~19 + 10 per lane before the kernels existed; the counts above are
+# the implemented formulation's (its SASS executes 91.5 for C5: profiles/fp64_instr.json).
+def fp64_instr_per_bin_update(limiter: int, P: int) -> float:
     if limiter == W.LIM_UPWIND:
-        primal = 5.0          # F = C n_up (1), update (2), mu3 FMA (2)
-        lane = 7.0            # Fdot = Cdot n_up + C ndot_up (3), update (2), mu3dot (2)
-        return primal + lane * P
-    primal = 12.0             # d (1), psi = 2ab/(a+b) (4), F = C n_up + kap psi (3), update (2), mu3 (2)
-    face_t = 8.0 if P else 0  # psi partials pa, pb (6) + g = n_up + beta psi (2), once per face
-    lane = 13.0               # ddot (1), pa adot + pb bdot (3), Fdot (5), update (2), mu3dot (2)
-    return primal + face_t + lane * P
+        return 6.0 + (1.0 if P else 0.0) + 5.0 * P
+    return 15.0 + (10.0 if P else 0.0) + 7.0 * P
 
 
 # ----------------------------------------------------------------------------------------
@@ -213,6 +223,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 streaming entry")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="C5: 4096 simulations in total (strong) or per GPU (weak)")
+    ap.add_argument("--quick", action="store_true", help="skip the per-config, sweep and 2D entries")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
@@ -321,14 +334,28 @@ def main():
                      kernel=kname, bytes_per_bin_update=bytes_per,
                      peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s", kernel_ms=kms)
         else:
-            f = flops_per_bin_update(w.limiter, P)
+            f = fp64_instr_per_bin_update(w.limiter, P)
             achieved = f * bu_local / (kms * 1e-3) / 1e12
             sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-            peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12     # FP64 FMA lanes x SMs x 2 flops x max SM clock
-            r = dict(bound="alu", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak, traffic=None,
-                     kernel="k_cluster" if info["kernel"] == pb.KERNEL_CLUSTER else "k_resident",
-                     flops_per_bin_update=f,
-                     peak_source=f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {sm_max:.0f} MHz", kernel_ms=kms)
+            nominal = 148 * 64 * sm_max * 1e6 / 1e12      # FP64 lanes x SMs x max SM clock (instr/s)
+            peak, src = nominal, f"derived: 148 SMs x 64 FP64 lanes/clk x {sm_max:.0f} MHz (no DFMA measurement)"
+            if dfma_tflops and dfma_tflops > 0:
+                peak, src = dfma_tflops / 2.0, "DFMA microbenchmark in this run (libpbe_mb.so), FMA = 1 instruction"
+            kname = "k_cluster" if info["kernel"] == pb.KERNEL_CLUSTER else (
+                "k_resident_ws" if info.get("warp_specialized") else "k_resident")
+            r = dict(bound="alu", achieved=achieved, peak=peak, unit="FP64 Tinst/s", frac=achieved / peak, traffic=None,
+                     kernel=kname, fp64_instr_per_bin_update=f, peak_source=src, peak_nominal=nominal, kernel_ms=kms)
+            fi = os.path.join(ROOT, "profiles", "fp64_instr.json")
+            if os.path.exists(fi):
+                try:
+                    e = json.load(open(fi)).get(kname)
+                    if e:
+                        r["sass_fp64_instr_per_bin_update"] = e["sass_fp64_instr_per_bin_update"]
+                        r["frac_sass"] = e["sass_fp64_instr_per_bin_update"] * bu_local / (kms * 1e-3) / 1e12 / peak
+                        r["ncu_fp64_pipe_active"] = e.get("ncu_fp64_pipe_active")
+                        r["sass_source"] = e["source"]
+                except Exception:
+                    pass
         if r.get("kernel") == "k_stream_tb":
             # temporal blocking moves 16 B per bin per HBM pass of spp steps, so HBM is not its bound;
             # report where it stands against the plain-streaming ceiling as well
@@ -347,6 +374,16 @@ def main():
                 pass
         return r
 
+    # ---- FP64 roofline denominator, measured on this GPU first ---------------------------------------
+    dfma_tflops = None
+    try:
+        import ctypes as C
+        mbl = C.CDLL(os.path.join(ROOT, "paper_2411_00742_b200", "libpbe_mb.so"))
+        mbl.pbe_mb_dfma_tflops.restype = C.c_double
+        dfma_tflops = float(mbl.pbe_mb_dfma_tflops(local_rank, 5))
+    except Exception:
+        pass
+
     # ---- main measurement ----------------------------------------------------------------------------
     clocks = ClockSampler(local_rank)
     ms, bu_local, kms = measure(ctx, w, n0_dev, ts, gather=True, clocks=clocks)
@@ -361,13 +398,7 @@ def main():
     info = ctx.last_run_info()
     value = bu_total / (ms * 1e-3)
     roof = roofline(w, info, bu_local, kms, args.workload)
-    try:
-        import ctypes as C
-        mbl = C.CDLL(os.path.join(ROOT, "paper_2411_00742_b200", "libpbe_mb.so"))
-        mbl.pbe_mb_dfma_tflops.restype = C.c_double
-        roof["dfma_microbench_tflops"] = float(mbl.pbe_mb_dfma_tflops(local_rank, 5))
-    except Exception:
-        pass
+    roof["dfma_microbench_tflops"] = dfma_tflops
 
     # ---- e2e through the C ABI with pinned host buffers ------------------------------------------
     e2e = None
@@ -382,14 +413,15 @@ def main():
                     steps=torch.empty(S, dtype=torch.int64).pin_memory().numpy(),
                     loss=torch.empty(S, dtype=torch.float64).pin_memory().numpy())
         grad_h = torch.empty((S, max(P, 1)), dtype=torch.float64).pin_memory().numpy()
+        trec_h = torch.empty((S, M, max(P, 1), 5), dtype=torch.float64).pin_memory().numpy() if P else None
         h2d = n0_h.nbytes + c0_h.nbytes + (ts_h.nbytes if ts_h is not None else 0) + (tg_h.nbytes if tg_h is not None else 0)
-        d2h = sum(v.nbytes for v in outh.values()) + (S * P * 8 if P else 0)
+        d2h = sum(v.nbytes for v in outh.values()) + (grad_h.nbytes + trec_h.nbytes if P else 0)
 
         def e2e_step():
             ctx.run_batch(n0_h, c0_h, ts_h, tg_h, stream=stream)
             ctx.moments(out=outh)
             if P:
-                ctx.tangents(out=dict(grad=grad_h))
+                ctx.tangents(out=dict(grad=grad_h, tangents=trec_h))     # gradient + every tangent record
         e2e_step()
         barrier(); torch.cuda.synchronize(dev)
         ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -406,7 +438,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms2 = float(t[0])
         e2e = dict(value=bu_total / (ms2 * 1e-3), unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
-                   ms_per_step=ms2, host_buffers="pinned", api="C ABI pbe_run_batch(n0_on_device=0) + pbe_moments")
+                   ms_per_step=ms2, host_buffers="pinned",
+                   api="C ABI pbe_run_batch(n0_on_device=0) + pbe_moments + pbe_tangents (records, loss, gradient, "
+                       "tangent records)")
 
     # ---- secondary (1 GPU): the C4 10^6-bin batch through the HBM-streaming kernel ----------------
     secondary = None
@@ -480,6 +514,85 @@ def main():
                      note="forward-mode tangents need 100 passes of 10 lanes (tools/next3_time.py: 205x slower)")
         del n03
 
+    # ---- strong scaling on one GPU: the rank-0 shard of W = 2, 4, 8 GPUs (BASELINE config 5 as written) --
+    strong_pred = None
+    if world == 1 and args.workload == "c5" and args.scaling == "strong" and not args.quick:
+        rows = []
+        for Wn in (2, 4, 8):
+            wsh = wg.subset(D.shard(wg.n_sims, 0, Wn))
+            ctxs = pb.context_for(wsh, device=local_rank)
+            n0s = torch.from_numpy(np.ascontiguousarray(wsh.n0)).to(dev)
+            ms_s, bu_s, kms_s = measure(ctxs, wsh, n0s, ts, gather=False)
+            ctxs.close()
+            rows.append(dict(gpus=Wn, sims_per_gpu=int(wsh.n_sims), ms_per_step=ms_s,
+                             predicted_efficiency=ms / (Wn * ms_s)))
+        strong_pred = dict(rows=rows, note="T(4096 sims, 1 GPU) / (W x T(4096/W sims, 1 GPU)): a shard runs no "
+                                          "collective during the march (one allgather of per-sim records after it)")
+
+    # ---- C1-C3 and the C4 bin sweep beside the oracle on one host core (same inputs) -------------------
+    def oracle_1core(wo, steps_cap=None):
+        import oracle
+        if steps_cap:
+            wo = W.replace(wo, n_steps=steps_cap)
+        t0 = time.perf_counter()
+        r = oracle.run(wo, threads=1, want_n=False)
+        dt = time.perf_counter() - t0
+        return float(wo.N) * float(np.sum(r["steps"])) / dt, dt, int(np.sum(r["steps"]))
+
+    cases, sweep = None, None
+    if world == 1 and rank == 0 and not args.quick:
+        cases = {}
+        for name, wc, what in (("c1", W.c1_growth(W.LIM_VANLEER, M=1000), "growth, constant G, fixed dt"),
+                               ("c2", W.c2_dissolution(), "dissolution, polynomial c*, T ramp"),
+                               ("c3", W.c3_cycling(), "temperature cycling, 10^5 steps")):
+            ctxc = pb.context_for(wc, device=local_rank)
+            n0c = torch.from_numpy(np.ascontiguousarray(wc.n0)).to(dev)
+            msc, buc, kmsc = measure(ctxc, wc, n0c, wc.t_samples, gather=False)
+            infoc = ctxc.last_run_info()
+            ctxc.close()
+            nst = buc / wc.N
+            orate, osec, _ = oracle_1core(wc)
+            cases[name] = dict(workload=what, bins=wc.N, sims=1, steps=int(round(nst)), ms=msc,
+                               us_per_step=1e3 * msc / nst, value=buc / (msc * 1e-3), unit=UNIT,
+                               kernel=infoc["kernel"], threads_per_cta=infoc["threads_per_cta"],
+                               oracle_1core=orate, oracle_seconds=osec, speedup_vs_oracle_1core=buc / (msc * 1e-3) / orate,
+                               note="latency-bound: one simulation is one CTA; us/step is the figure of merit")
+        sweep = []
+        for N in (1000, 10000, 100000, 1000000):
+            orate = None
+            for b in (1, 64):
+                w4 = W.c4_sweep(N, batch=b, n_steps=1000)
+                ctx4 = pb.context_for(w4, device=local_rank)
+                n04 = torch.from_numpy(np.ascontiguousarray(w4.n0)).to(dev)
+                ms4, bu4, _ = measure(ctx4, w4, n04, None, gather=False)
+                i4 = ctx4.last_run_info()
+                ctx4.close()
+                if orate is None:
+                    cap = int(min(1000, max(20, 2e7 // N)))
+                    orate, _, osteps = oracle_1core(W.c4_sweep(N, batch=1, n_steps=1000), steps_cap=cap)
+                sweep.append(dict(bins=N, sims=b, steps=1000, ms=ms4, us_per_step=1e3 * ms4 / 1000,
+                                  value=bu4 / (ms4 * 1e-3), unit=UNIT, kernel=i4["kernel"],
+                                  steps_per_pass=i4["steps_per_pass"], oracle_1core=orate,
+                                  oracle_note=(f"one simulation, first {osteps} of the 1000 steps on one core "
+                                               "(per-step cost is constant in steps mode: rate extrapolated)"
+                                               if osteps < 1000 else "one simulation, all 1000 steps, one core")))
+
+    # ---- NEXT-1 (1 GPU): the paper's 2D model, 6000 x 3000 grid, 4 simulations ------------------------
+    next1 = None
+    if world == 1 and args.workload == "c5" and not args.quick:
+        w2 = W.c2d_base(6000, 3000, n_sims=4)
+        w2.n_steps = 100
+        w2.t_samples = np.array([1.0])
+        ctx2 = pb.context_for(w2, device=local_rank)
+        n02 = torch.from_numpy(np.ascontiguousarray(w2.n0)).to(dev)
+        ms2d, bu2d, kms2d = measure(ctx2, w2, n02, None, gather=False)
+        i2 = ctx2.last_run_info()
+        ctx2.close()
+        next1 = dict(workload="NEXT-1 2D base case 6000 x 3000 (Godunov splitting, van Leer), 4 sims, 100 uncapped "
+                              "CFL steps", value=bu2d / (ms2d * 1e-3), unit="cell-updates/s", ms_per_step=ms2d,
+                     roofline=roofline(w2, i2, bu2d, kms2d, "c2d"), kernel=i2)
+        del n02
+
     # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -491,12 +604,15 @@ def main():
         cfg = dict(desc)
         cfg.update(parallelism=(f"sims sharded round-robin over {world} GPUs; NCCL allgather of per-sim records"
                                 if world > 1 else "1 GPU"), l2="flushed between timed iterations (512 MiB write)",
+                   scaling=args.scaling,
                    steps_per_sim_mean=bu_local / (w.N * max(w.N2, 1)) / max(w.n_sims, 1), kernel=info)
         line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
-                    ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                    ms_per_step=ms, higher_is_better=True, scaling=args.scaling if args.workload == "c5" else "weak",
+                    vs_baseline=None, dtype="f64",
                     data="synthetic (seeded; DESIGN.md input recipe)", config=cfg, roofline=roof,
                     cpu_baseline=cpu, e2e=e2e, gpu_launches=int(info["launches"]) * args.steps, clocks=clk,
-                    secondary=secondary, next3=next3, next4=next4)
+                    secondary=secondary, next3=next3, next4=next4, next1=next1,
+                    strong_scaling_prediction=strong_pred, cases=cases, c4_sweep=sweep)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -240,7 +240,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
     __shared__ double2 s_poly[MAXTH][32];            // POLY fast path: lane l's dual coefficient
     __shared__ double s_th[MAXTH], s_sol[3], s_seed[MAXP * (MAXTH + 3)];
 
-    const int s = blockIdx.x;
+    // lane groups (kp.G CTAs per simulation, e.g. the last partial wave of a batch split in two):
+    // CTA b marches simulation kp.sim0 + b / G with tangent lanes [lane0, lane0 + nl) of kp.P;
+    // every group recomputes the primal march bitwise identically and group 0 writes its outputs
+    const int s = kp.sim0 + (int)blockIdx.x / kp.G;
+    const int grp = (int)blockIdx.x % kp.G;
+    const int lane0 = grp * P;
+    const int nl = max(0, min(P, kp.P - lane0));             // lanes of this CTA in use
+    const bool primal_out = grp == 0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool scal = warp == 0;             // the scalar warp
     const int bt = tid - 32, bw = warp - 1;  // bin thread / bin warp (bin warps only)
@@ -262,12 +269,12 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
         const double* th = kp.theta + (size_t)s * kp.n_params;
         for (int j = tid; j < kp.n_params; j += NT) s_th[j] = th[j];
         for (int j = tid; j < kp.n_sol; j += NT) s_sol[j] = kp.sol[j];
-        for (int j = tid; j < kp.P * nsd; j += NT) s_seed[j] = kp.seed[j];
+        for (int j = tid; j < nl * nsd; j += NT) s_seed[j] = kp.seed[(size_t)lane0 * nsd + j];
         for (int e = tid; e < MAXTH * 32; e += NT) {     // lane l seeds direction l - 2 (lanes 0/1: c, t)
             const int j = e >> 5, l = e & 31;
             const bool on = j < kp.n_params;
-            const bool seeded = on && l >= 2 && l - 2 < kp.P;
-            s_poly[j][l] = make_double2(on ? th[j] : 0.0, seeded ? kp.seed[(size_t)(l - 2) * nsd + j] : 0.0);
+            const bool seeded = on && l >= 2 && l - 2 < nl;
+            s_poly[j][l] = make_double2(on ? th[j] : 0.0, seeded ? kp.seed[(size_t)(lane0 + l - 2) * nsd + j] : 0.0);
         }
     }
     double x[K];                             // primal bins (bin warps)
@@ -348,9 +355,10 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
     int m, status, landing;
     bool go, last_ok, sample;
     const double* kT = kp.knot_T + (size_t)s * kp.knotT_stride;
-    const int seedl = (lane >= 2 && lane - 2 < kp.P) ? lane - 2 : -1;   // lanes >= kp.P carry 0
+    const int seedl = (lane >= 2 && lane - 2 < nl) ? lane - 2 : -1;   // lanes >= nl carry 0
     const KinLoaderS KLS{s_th, s_sol, s_seed, seedl, kp.n_params, nsd};
-    const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, seedl, kp.n_params, nsd};
+    const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, seedl >= 0 ? lane0 + seedl : -1,
+                       kp.n_params, nsd};
     const KinCache KC = kin_smem ? kin_cache(kp, KLS, kT) : kin_cache(kp, KL, kT);
     const bool poly_fast = kin_smem && kp.law == LAW_POLY && KC.const_T;
     // kinetics + time step of the next step, Jacobian-seeded duals (rows a1, a2) -> s_step
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
             }
         } else if (kp.law == LAW_POLY && kp.n_params > MAXTH) {
             const D1 S = supersaturation(kp, LDR, kT, KC, tD, cD, T);
-            G = poly_long_warp_seeded<P>(kp.theta + (size_t)s * kp.n_params, kp.seed, nsd, 0, kp.P, kp.n_params, S,
+            G = poly_long_warp_seeded<P>(kp.theta + (size_t)s * kp.n_params, kp.seed, nsd, lane0, nl, kp.n_params, S,
                                          seedl);
         } else {
             const D1 S = supersaturation(kp, LDR, kT, KC, tD, cD, T);
@@ -402,7 +410,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
         bool need_kin = go;
         if (n >= 0) {
             const double mu3n = total(3);
-            const double cn = c - kp.rho_kv * (mu3n - mu3p);          // eq-discrete_mass_balance
+            const double cn = __dsub_rn(c, __dmul_rn(kp.rho_kv, __dsub_rn(mu3n, mu3p)));   // eq-discrete_mass_balance
             need_kin = false;
             if (s_bad == n) { status = ST_NEG; go = false; last_ok = false; }
             else if (cn < 0.0) { status = ST_INFEAS; go = false; last_ok = false; }
@@ -410,7 +418,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
                 c = cn; mu3p = mu3n;
                 t = landing ? kp.t_samples[m] : t + dt;
                 ++nstep;
-                if (sample && lane == 0) {
+                if (sample && lane == 0 && primal_out) {
                     const int mr = steps_mode ? 0 : m;
                     double* r = kp.rec + ((size_t)s * kp.M + mr) * 6;
                     r[0] = t; r[1] = c; r[2] = total(0); r[3] = total(1); r[4] = total(2); r[5] = mu3n;
@@ -490,14 +498,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
     // lane-parallel tangent scalars at the start of step n (after barrier 1): cdot^n, tdot^n
     auto tangent_scalars = [&]() __attribute__((always_inline)) {
         const double m3 = tsum(3);
-        cdl = cdl - kp.rho_kv * (m3 - mu3d);                           // tangent of the mass balance
+        cdl = __dsub_rn(cdl, __dmul_rn(kp.rho_kv, __dsub_rn(m3, mu3d)));   // tangent of the mass balance
         mu3d = m3;
         tdl = lnd_prev ? 0.0 : tdl + dtdl;                             // t := t_m exactly on landing
     };
     // tangent record of sample step n - 1 (scalar warp, after tangent_scalars)
     auto tangent_record = [&](const WsMsg& Mp) __attribute__((always_inline)) {
-        if (smp_prev && Mp.last_ok && lane < kp.P) {
-            double* rt = kp.trec + (((size_t)s * kp.M + m_prev) * kp.P + lane) * 5;
+        if (smp_prev && Mp.last_ok && lane < nl) {
+            double* rt = kp.trec + (((size_t)s * kp.M + m_prev) * kp.P + lane0 + lane) * 5;
             rt[0] = cdl; rt[1] = tsum(0); rt[2] = tsum(1); rt[3] = tsum(2); rt[4] = mu3d;
         }
     };
@@ -610,22 +618,22 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
 #pragma unroll
         for (int k = 0; k < K; ++k) x[k] = sx[k * NB + bt];
     }
-    if (!scal && kp.n_final) {
+    if (!scal && kp.n_final && primal_out) {
 #pragma unroll
         for (int k = 0; k < K; ++k) { const int i = i0 + k; if (i < N) kp.n_final[(size_t)s * N + i] = x[k]; }
     }
     if (!scal && kp.ndot_final) {
 #pragma unroll
         for (int p = 0; p < P; ++p)
-            if (p < kp.P) {
+            if (p < nl) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const int i = i0 + k;
-                    if (i < N) kp.ndot_final[((size_t)s * kp.P + p) * N + i] = y[p][k];
+                    if (i < N) kp.ndot_final[((size_t)s * kp.P + lane0 + p) * N + i] = y[p][k];
                 }
             }
     }
-    if (tid == 0) { kp.status[s] = s_ch.status; kp.steps[s] = s_ch.nstep; }
+    if (tid == 0 && primal_out) { kp.status[s] = s_ch.status; kp.steps[s] = s_ch.nstep; }
     // ---- loss and gradient from the sample records (R-23), in sample order ------------------
     __syncthreads();                       // records are complete and visible
     if (scal) {
@@ -644,7 +652,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
             }
             const double rms_c = sqrt(sc2 / kp.M), rms_L = sqrt(sl2 / kp.M);
             const int Mr = steps_mode ? 1 : kp.M;
-            const int pg = lane < kp.P ? lane : 0;
+            const int pg = lane0 + (lane < nl ? lane : 0);
             for (int mr = 0; mr < Mr; ++mr) {
                 const double* r = kp.rec + ((size_t)s * kp.M + mr) * 6;
                 const double* rt = kp.trec + (((size_t)s * kp.M + mr) * kp.P + pg) * 5;
@@ -655,8 +663,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_ws(const KParams kp) {
                 gacc += 2.0 * (rc / rms_c) * rt[0] + 2.0 * (rL / rms_L) * Lbd;
             }
         }
-        if (lane == 0 && kp.loss) kp.loss[s] = (has_target && ok) ? loss : qnan;
-        if (lane < kp.P && kp.grad) kp.grad[(size_t)s * kp.P + lane] = (has_target && ok) ? gacc : qnan;
+        if (lane == 0 && kp.loss && primal_out) kp.loss[s] = (has_target && ok) ? loss : qnan;
+        if (lane < nl && kp.grad) kp.grad[(size_t)s * kp.P + lane0 + lane] = (has_target && ok) ? gacc : qnan;
     }
 }
 

@@ -78,6 +78,7 @@ struct pbe_ctx_s {
     int resident_k = 0;      // env PBE_RESIDENT_K: preferred bins per thread (0 = heuristic)
     bool ws = true;          // env PBE_WS=0: lockstep k_resident instead of k_resident_ws for P >= 1
     int ws_variant = 0;      // env PBE_WS_VARIANT: k_resident_ws tuning variant (A/B only)
+    bool ws_tail = true;     // env PBE_WS_TAIL=0: no half-lane CTAs for the last partial wave
     bool temporal_block = true;  // NEXT-4 temporal blocking for uncapped-CFL steps mode in
                                  // k_stream (1.27x plain streaming on 64 x 1e6); env
                                  // PBE_TEMPORAL_BLOCK=0 selects plain streaming
@@ -133,7 +134,7 @@ struct WsVariant {
 #define WV(P, K, T) WsVariant{P, K, T, &pbe::k_resident_ws<P, K, T, false, false, 0>, false, 0}
 #define WVX(P, K, T, XS, HALF, LAG, TAG) WsVariant{P, K, T, &pbe::k_resident_ws<P, K, T, XS, HALF, LAG>, XS, TAG}
 const WsVariant kResidentWS[] = {
-    WV(8, 9, 64), WV(8, 9, 128), WV(8, 9, 256),
+    WV(8, 9, 64), WV(8, 9, 128), WV(8, 9, 256), WV(4, 9, 64), WV(4, 9, 128), WV(4, 9, 256),
     WVX(8, 9, 256, true, false, 2, 1), WVX(8, 9, 256, true, true, 2, 2), WVX(8, 9, 256, true, false, 0, 3),
     WVX(8, 9, 256, true, true, 0, 4), WVX(8, 9, 256, false, true, 2, 5), WVX(8, 9, 256, false, false, 2, 6),
 };
@@ -685,6 +686,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (const char* e = getenv("PBE_RESIDENT_K")) ctx->resident_k = atoi(e);
     if (const char* e = getenv("PBE_WS")) ctx->ws = atoi(e) != 0;
     if (const char* e = getenv("PBE_WS_VARIANT")) ctx->ws_variant = atoi(e);
+    if (const char* e = getenv("PBE_WS_TAIL")) ctx->ws_tail = atoi(e) != 0;
     if (const char* e = getenv("PBE_TEMPORAL_BLOCK")) ctx->temporal_block = atoi(e) != 0;
     if (const char* e = getenv("PBE_2D_UNFUSED")) ctx->unfused_2d = atoi(e) != 0;
     ctx->device = device;
@@ -841,15 +843,38 @@ pbe_status pbe_run_batch(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t 
         const int nt = ws->nt;
         const size_t smem = ws->smem();
         CUDA_TRY(ctx, cudaFuncSetAttribute(ws->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // one CTA per simulation runs in waves of `sms` CTAs.  A last partial wave of at most
+        // sms/2 simulations runs as two half-lane CTAs per simulation instead (a second launch of
+        // the P/2-lane variant with kp.G = 2; results are bitwise the same), so the tail wave
+        // takes the time of a half-lane march: 512 sims on 148 SMs = 3 full waves + 68 x 2 CTAs
+        int sms = 148;
+        CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int tail = n_sims % sms;
+        const WsVariant* half = nullptr;
+        if (ctx->ws_tail && ws->P >= 2 && tail > 0 && 2 * tail <= sms) {
+            for (const auto& v : kResidentWS)
+                if (v.tag == 0 && v.P == ws->P / 2 && v.K == ws->K && v.nt == ws->nt) half = &v;
+        }
+        const int n_full = half ? n_sims - tail : n_sims;
         kp.G = 1;
+        kp.sim0 = 0;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-        ws->fn<<<n_sims, nt, smem, st>>>(kp);
+        if (n_full > 0) ws->fn<<<n_full, nt, smem, st>>>(kp);
         CUDA_TRY(ctx, cudaGetLastError());
+        if (half) {
+            const size_t hs = half->smem();
+            CUDA_TRY(ctx, cudaFuncSetAttribute(half->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
+            KParams kh = kp;
+            kh.G = 2;
+            kh.sim0 = n_full;
+            half->fn<<<2 * tail, nt, hs, st>>>(kh);
+            CUDA_TRY(ctx, cudaGetLastError());
+        }
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
         ctx->info.kernel = PBE_KERNEL_RESIDENT;
-        ctx->info.launches = 1;
+        ctx->info.launches = (n_full > 0) + (half != nullptr);
         ctx->info.threads_per_cta = nt;
-        ctx->info.ctas = n_sims;
+        ctx->info.ctas = n_full + (half ? 2 * tail : 0);
         ctx->info.cluster = 1;
         ctx->info.bins_per_thread = ws->K;
         ctx->info.warp_specialized = 1;

@@ -47,6 +47,7 @@ struct KParams {
     // batch
     int n_sims, M, P;       // P = tangent lanes of a simulation
     int G;                  // lane groups per simulation (CTAs per simulation)
+    int sim0;               // first simulation of the launch (k_resident_ws tail launches)
     const double* n0; long long n0_stride;
     const double* c0;       // [S]
     const double* t_samples;// [M]
@@ -77,28 +78,34 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // D1: value + one tangent (this lane's direction).  Divisions use rcp_nr (<= ~1 ulp off the
 // correctly rounded quotient, no slow path); operands are c*, S-like ratios and |G| > 1e-300.
 // ------------------------------------------------------------------------------------
+// Every operation is an explicitly rounded intrinsic (no FMA contraction left to the compiler),
+// so the primal value of an expression never depends on the code around it: kernels that
+// evaluate the same kinetics with different tangent seedings (k_resident_ws full and half-lane
+// CTAs) take bitwise identical primal decisions.
 struct D1 { double v, d; };
 __device__ __forceinline__ D1 mk(double v, double d = 0.0) { return D1{v, d}; }
-__device__ __forceinline__ D1 operator+(D1 a, D1 b) { return {a.v + b.v, a.d + b.d}; }
-__device__ __forceinline__ D1 operator-(D1 a, D1 b) { return {a.v - b.v, a.d - b.d}; }
+__device__ __forceinline__ D1 operator+(D1 a, D1 b) { return {__dadd_rn(a.v, b.v), __dadd_rn(a.d, b.d)}; }
+__device__ __forceinline__ D1 operator-(D1 a, D1 b) { return {__dsub_rn(a.v, b.v), __dsub_rn(a.d, b.d)}; }
 __device__ __forceinline__ D1 operator-(D1 a) { return {-a.v, -a.d}; }
-__device__ __forceinline__ D1 operator*(D1 a, D1 b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+__device__ __forceinline__ D1 operator*(D1 a, D1 b) {
+    return {__dmul_rn(a.v, b.v), __fma_rn(a.d, b.v, __dmul_rn(a.v, b.d))};
+}
 __device__ __forceinline__ D1 operator/(D1 a, D1 b) {
-    const double r = rcp_nr(b.v), q = a.v * r;
-    return {q, (a.d - q * b.d) * r};
+    const double r = rcp_nr(b.v), q = __dmul_rn(a.v, r);
+    return {q, __dmul_rn(__fma_rn(-q, b.d, a.d), r)};
 }
-__device__ __forceinline__ D1 operator+(D1 a, double b) { return {a.v + b, a.d}; }
-__device__ __forceinline__ D1 operator-(D1 a, double b) { return {a.v - b, a.d}; }
-__device__ __forceinline__ D1 operator+(double a, D1 b) { return {a + b.v, b.d}; }
-__device__ __forceinline__ D1 operator-(double a, D1 b) { return {a - b.v, -b.d}; }
-__device__ __forceinline__ D1 operator*(D1 a, double b) { return {a.v * b, a.d * b}; }
-__device__ __forceinline__ D1 operator*(double a, D1 b) { return {a * b.v, a * b.d}; }
+__device__ __forceinline__ D1 operator+(D1 a, double b) { return {__dadd_rn(a.v, b), a.d}; }
+__device__ __forceinline__ D1 operator-(D1 a, double b) { return {__dsub_rn(a.v, b), a.d}; }
+__device__ __forceinline__ D1 operator+(double a, D1 b) { return {__dadd_rn(a, b.v), b.d}; }
+__device__ __forceinline__ D1 operator-(double a, D1 b) { return {__dsub_rn(a, b.v), -b.d}; }
+__device__ __forceinline__ D1 operator*(D1 a, double b) { return {__dmul_rn(a.v, b), __dmul_rn(a.d, b)}; }
+__device__ __forceinline__ D1 operator*(double a, D1 b) { return {__dmul_rn(a, b.v), __dmul_rn(a, b.d)}; }
 __device__ __forceinline__ D1 operator/(double a, D1 b) {
-    const double r = rcp_nr(b.v), q = a * r;
-    return {q, -q * b.d * r};
+    const double r = rcp_nr(b.v), q = __dmul_rn(a, r);
+    return {q, __dmul_rn(__dmul_rn(-q, b.d), r)};
 }
-__device__ __forceinline__ D1 dexp(D1 a) { const double e = exp(a.v); return {e, e * a.d}; }
-__device__ __forceinline__ D1 dlog(D1 a) { return {log(a.v), a.d / a.v}; }
+__device__ __forceinline__ D1 dexp(D1 a) { const double e = exp(a.v); return {e, __dmul_rn(e, a.d)}; }
+__device__ __forceinline__ D1 dlog(D1 a) { return {log(a.v), __ddiv_rn(a.d, a.v)}; }
 // |x| with d|x| = sgn(x) dx, sgn(0) = 0 (R-20)
 __device__ __forceinline__ D1 dabs(D1 a) { return a.v > 0.0 ? a : (a.v < 0.0 ? -a : D1{0.0, 0.0}); }
 
@@ -289,7 +296,7 @@ __device__ __forceinline__ StepScalars time_step(const KParams& kp, D1 G, D1 t, 
         C = mk(0.0);
     }
     if (!steps_mode) {
-        if (t.v + dt.v >= tn - 1e-9 * dt.v) {
+        if (__dadd_rn(t.v, dt.v) >= __dsub_rn(tn, __dmul_rn(1e-9, dt.v))) {
             const D1 dtl = tn - t;
             const D1 Cl = G * dtl * kp.inv_dL;
             if (fabs(Cl.v) <= 1.0) { dt = dtl; C = Cl; r.landing = true; }

@@ -490,3 +490,24 @@ def test_resident_kinds_steps_mode_and_lane_counts(resident_kind):
     g, o = _check(w, mode=oracle.MODE_DUAL)
     _expect_kind(g, resident_kind)
     assert np.all(g["steps"] == 77) and np.any(g["ndot_final"] != 0.0)
+
+
+def test_tail_wave_half_lane_ctas_bitwise():
+    """A last partial wave of <= 74 simulations runs as two 4-lane CTAs per simulation (second
+    launch, kp.G = 2).  Results must be bitwise those of the one-CTA march of the same simulation
+    (the primal is recomputed identically; every tangent reduction has the same order)."""
+    w = W.c5_ensemble(n_sims=148, N=300, t_max=15.0, M=15)
+    g_full = _gpu(w)                                     # 148 sims: one full wave, no split
+    assert g_full["info"]["launches"] == 1 and g_full["info"]["ctas"] == 148
+    for sims in ([17], [3, 90, 147]):                    # tails of 1 and 3 simulations: split
+        g = _gpu(w.subset(sims))
+        assert g["info"]["launches"] == 1 and g["info"]["ctas"] == 2 * len(sims)
+        for k in ("samples", "tsamples", "n_final", "ndot_final", "loss", "grad", "status", "steps"):
+            assert np.array_equal(g[k], g_full[k][sims], equal_nan=True), k
+    w150 = W.c5_ensemble(n_sims=150, N=300, t_max=15.0, M=15)
+    g150 = _gpu(w150)                                    # 148 full CTAs + 2 x 2 half CTAs
+    assert g150["info"]["launches"] == 2 and g150["info"]["ctas"] == 152
+    o = oracle.run(w150.subset([0, 148, 149]), mode=oracle.MODE_DUAL, threads=3)
+    gs = {k: g150[k][[0, 148, 149]] for k in ("samples", "tsamples", "status", "steps")}
+    _cmp_samples(gs, o)
+    _cmp_tangents(gs, o)

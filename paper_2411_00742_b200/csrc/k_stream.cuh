@@ -72,6 +72,11 @@ struct StreamParams {
     int* active;            // [3] rotating counters of simulations still marching
     int* final_buf;         // [S] buffer (0/1) holding each simulation's final state
     const unsigned long long* nscale_bits;  // [S] max(n0_s) as uint64 bits (non-negative)
+    // dynamic tile scheduling (k_stream<P, true>): per-step tile counters, per-simulation step
+    // coefficients published by the simulation's owner warp, and the step they are valid for
+    unsigned* tile_ctr;     // [3] rotating per-step counters
+    void* coef;             // [S] SimCoef<P>
+    unsigned* coef_step;    // [S] step index of coef[s] (0xffffffff before the first publication)
 };
 
 // ---- PTX helpers ----------------------------------------------------------------------
@@ -97,6 +102,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
@@ -218,7 +226,14 @@ __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int R
     }
 }
 
-template <int P>
+// DYN = false: every CTA streams a static contiguous tile range and replicates the scalar phase of
+// the <= STREAM_MAXS simulations it touches.  DYN = true (default): tiles are handed out by a per-
+// step atomic counter (a CTA that finishes early takes more: no imbalance wait at the grid barrier);
+// simulation s is owned by CTA s % G (slot s / G), whose warp publishes the step coefficients to
+// global memory with a release flag that the producers acquire before streaming s's tiles.  Tile
+// partials keep their [s][tile][warp] slots, so every sum keeps its fixed order (bitwise the same
+// results as the static schedule).
+template <int P, bool DYN>
 __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(const StreamParams sp) {
     constexpr int V = 1 + P;
     constexpr int K = StreamCfg<V>::K;
@@ -233,16 +248,33 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
     const unsigned G = gridDim.x;
     const double L_half = kp.L_lo + 0.5 * kp.dL;
 
-    // static tile range of this CTA
-    const long long t_lo = (sp.n_tiles * blockIdx.x) / G;
-    const long long t_hi = (sp.n_tiles * (blockIdx.x + 1)) / G;
-    const int s_lo = (int)(t_lo / sp.T_sim);
-    const int ns = (t_hi > t_lo) ? (int)((t_hi - 1) / sp.T_sim) - s_lo + 1 : 0;
+    // static tile range of this CTA (DYN: only the owned simulations s = blockIdx + slot G)
+    const long long t_lo = DYN ? 0 : (sp.n_tiles * blockIdx.x) / G;
+    const long long t_hi = DYN ? 0 : (sp.n_tiles * (blockIdx.x + 1)) / G;
+    const int s_lo = DYN ? 0 : (int)(t_lo / sp.T_sim);
+    const int ns = DYN ? (kp.n_sims > (int)blockIdx.x ? (kp.n_sims - (int)blockIdx.x + (int)G - 1) / (int)G : 0)
+                       : ((t_hi > t_lo) ? (int)((t_hi - 1) / sp.T_sim) - s_lo + 1 : 0);
+    auto sim_of_slot = [&](int slot) { return DYN ? (int)blockIdx.x + slot * (int)G : s_lo + slot; };
+    auto is_owner = [&](int slot) { return DYN || (long long)(s_lo + slot) * sp.T_sim >= t_lo; };
 
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) unsigned long long s_full[STG], s_empty[STG];
     __shared__ SimCoef<P> s_coef[STREAM_MAXS];
     __shared__ double s_clip[STREAM_MAXS];
+    __shared__ SimCoef<P> s_cfs[DYN ? STG : 1];      // DYN: coefficients of the tile in each stage
+    __shared__ long long s_tile[DYN ? STG : 1];      // DYN: tile id in each stage (-1: end of step)
+    SimCoef<P>* gcoef = reinterpret_cast<SimCoef<P>*>(sp.coef);
+    // DYN: the owner publishes slot's coefficients of step `step` (every lane has them in s_coef)
+    auto publish = [&](int slot, unsigned step) {
+        if (!DYN) return;
+        __syncwarp();
+        const int s = sim_of_slot(slot);
+        if (lane == 0) {
+            gcoef[s] = s_coef[slot];
+            __threadfence();
+            st_release(&sp.coef_step[s], step);
+        }
+    };
 
     // per-simulation scalar state: primal per slot (lane 0 copy), tangent per (slot, lane)
     struct SimPrimal { double c, t, mu3p, dt, loss, rms_c, rms_L; long long nstep; int m, status, landing, go; };
@@ -351,10 +383,64 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         badf = bf;
     };
 
+    // DYN: the totals of every owned simulation summed by all NWC consumer warps of the CTA (the
+    // sum is on the step's critical path: the other CTAs' producers wait for the coefficients).
+    // Warp w takes entries e with (e / 32) % NWC == w, lane l entries e % 32 == l, in increasing
+    // order; lanes combine by a fixed xor tree, warps in warp order: deterministic.
+    constexpr int NXV = 4 * V + 1;
+    __shared__ double s_wtot[DYN ? STREAM_MAXS : 1][DYN ? NWC : 1][DYN ? NXV : 1];
+    auto cta_partials = [&](int slot, bool sample) {
+        const int s = sim_of_slot(slot);
+        const double* pt = sp.part + (size_t)s * sp.T_sim * NWC * 5 * V;
+        const int ne = sp.T_sim * NWC;
+        double a[NXV];
+#pragma unroll
+        for (int x = 0; x < NXV; ++x) a[x] = 0.0;
+#pragma unroll 4
+        for (int e = warp * 32 + lane; e < ne; e += NWC * 32) {             // independent L2 loads
+            const double* q = pt + (size_t)e * 5 * V;
+            if (sample) {
+#pragma unroll
+                for (int x = 0; x < 4 * V; ++x) a[x] += q[x];
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) a[3 * V + v] += q[3 * V + v];
+            }
+            a[4 * V] += q[4 * V];
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int x = 0; x < NXV; ++x) a[x] += __shfl_xor_sync(0xffffffffu, a[x], off);
+        if (lane < NXV) {
+            double mine = 0.0;
+#pragma unroll
+            for (int x = 0; x < NXV; ++x) if (x == lane) mine = a[x];
+            s_wtot[slot][warp][lane] = mine;
+        }
+    };
+    auto cta_totals = [&](int slot, bool sample, double (&tot)[4], double (&totd)[4], double& badf) {
+        double a[NXV];
+#pragma unroll
+        for (int x = 0; x < NXV; ++x) a[x] = 0.0;
+        for (int w = 0; w < NWC; ++w)
+#pragma unroll
+            for (int x = 0; x < NXV; ++x) a[x] += s_wtot[slot][w][x];
+#pragma unroll
+        for (int km = 0; km < 4; ++km) {
+            const bool on = km == 3 || sample;
+            tot[km] = on ? a[km * V] : 0.0;
+            totd[km] = 0.0;
+#pragma unroll
+            for (int p = 0; p < P; ++p) if (p == pl && on) totd[km] = a[km * V + 1 + p];
+        }
+        badf = a[4 * V];
+    };
+
     // ---- scalar state init (one warp per simulation slot); mu3(n0) from the load kernel's
     //      per-tile partials (same layout and order as a step) ----------------------------
     if (warp < ns) {
-        const int slot = warp, s = s_lo + slot;
+        const int slot = warp, s = sim_of_slot(slot);
         double tot[4], totd[4], badf;
         sim_totals(s, false, tot, totd, badf);
         SimPrimal W{};
@@ -381,6 +467,7 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         } else {
             set_inactive(slot);
         }
+        publish(slot, 0u);
         __syncwarp();
         if (lane == 0) s_sp[slot] = W;
         s_st[slot][lane] = T;
@@ -401,6 +488,122 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         const double* src = src_sel ? sp.buf1 : sp.buf0;
         double* dst = src_sel ? sp.buf0 : sp.buf1;
         const unsigned long long q0 = qq;
+        if (DYN) {
+            if (producer) {
+                // ---- TMA producer: tiles from the step's atomic counter, in counter order ----------
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    unsigned long long q = q0;
+                    while (true) {
+                        long long t = (long long)atomicAdd(&sp.tile_ctr[n % 3], 1u);
+                        int s = 0;
+                        bool live = false;
+                        while (t < sp.n_tiles) {
+                            s = (int)(t / sp.T_sim);
+                            while (ld_acquire(&sp.coef_step[s]) != (unsigned)n) __nanosleep(20);
+                            if (gcoef[s].active) { live = true; break; }
+                            // inactive simulation: skip the rest of its tiles in one step
+                            atomicMax(&sp.tile_ctr[n % 3], (unsigned)((long long)(s + 1) * sp.T_sim));
+                            t = (long long)atomicAdd(&sp.tile_ctr[n % 3], 1u);
+                        }
+                        const int st = (int)(q % STG);
+                        if (q >= STG) mbar_wait(&s_empty[st], (unsigned)(((q / STG) - 1) & 1));
+                        ++q;
+                        if (!live) {                       // end of the step for this CTA
+                            s_tile[st] = -1;
+                            mbar_arrive(&s_full[st]);
+                            break;
+                        }
+                        s_cfs[st] = gcoef[s];
+                        s_tile[st] = t;
+                        const int j = (int)(t - (long long)s * sp.T_sim);
+                        const int b0 = j * TB, nb = min(TB, N - b0);
+                        const unsigned n_el = (unsigned)((nb + 4 + 1) & ~1);   // even -> 16-byte multiple
+                        mbar_expect_tx(&s_full[st], n_el * 8u * V);
+#pragma unroll
+                        for (int v = 0; v < V; ++v)
+                            bulk_g2s(smem + ((size_t)st * V + v) * RS, src + ((size_t)s * V + v) * sp.pitch + b0,
+                                     n_el * 8u, &s_full[st]);
+                    }
+                    qq = q;
+                }
+                qq = __shfl_sync(0xffffffffu, qq, 0);
+            } else {
+                // ---- consumers: whatever tile each stage holds, until the end marker ----------------
+                while (true) {
+                    const int st = (int)(qq % STG);
+                    mbar_wait(&s_full[st], (unsigned)((qq / STG) & 1));
+                    ++qq;
+                    const long long t = s_tile[st];
+                    if (t < 0) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&s_empty[st]);
+                        break;
+                    }
+                    const int s = (int)(t / sp.T_sim), j = (int)(t - (long long)s * sp.T_sim);
+                    const int b0 = j * TB, nb = min(TB, N - b0);
+                    const SimCoef<P> cf = s_cfs[st];
+                    const bool sample = cf.sample != 0;
+                    const double* sb = smem + (size_t)st * V * RS;
+                    double* drow = dst + (size_t)s * V * sp.pitch + b0 + 2;
+                    double acc[4][V];
+#pragma unroll
+                    for (int km = 0; km < 4; ++km)
+#pragma unroll
+                        for (int v = 0; v < V; ++v) acc[km][v] = 0.0;
+                    bool neg = false;
+#define PBE_SB(NEGV, LKV)                                                                                  \
+    for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)                                     \
+        stream_bins<P, K, NEGV, LKV>(sb, RS, g0, nb, b0, cf, vl, sample, L_half, kp.dL, drow, sp.pitch, acc, neg)
+                    const int lk = vl == LIM_VANLEER ? 1 : (vl == LIM_UPWIND ? 0 : 2);
+                    if (cf.C >= 0.0) {
+                        if (lk == 1) PBE_SB(false, 1); else if (lk == 0) PBE_SB(false, 0); else PBE_SB(false, 2);
+                    } else {
+                        if (lk == 1) PBE_SB(true, 1); else if (lk == 0) PBE_SB(true, 0); else PBE_SB(true, 2);
+                    }
+#undef PBE_SB
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_empty[st]);           // stage free for the producer
+                    bool bad = false;
+                    if (__any_sync(0xffffffffu, neg)) {
+                        const double thr = 1e-12 * __longlong_as_double((long long)sp.nscale_bits[s]);
+                        for (int g0 = (warp * 32 + lane) * K; g0 < nb; g0 += NWC * 32 * K)
+                            for (int k = 0; k < K && g0 + k < nb; ++k) {
+                                const double nn = drow[g0 + k];
+                                if (nn < 0.0) {
+                                    if (nn >= -thr) {
+                                        const double Lc = fma((double)(b0 + g0 + k), kp.dL, L_half);
+                                        const double w1 = kp.dL * Lc, w2 = w1 * Lc, w3 = w2 * Lc;
+#pragma unroll
+                                        for (int v = 0; v < V; ++v) {
+                                            const double yv = drow[(size_t)v * sp.pitch + g0 + k];
+                                            acc[3][v] -= w3 * yv;
+                                            if (sample) { acc[0][v] -= kp.dL * yv; acc[1][v] -= w1 * yv; acc[2][v] -= w2 * yv; }
+                                            drow[(size_t)v * sp.pitch + g0 + k] = 0.0;
+                                        }
+                                    } else {
+                                        bad = true;
+                                    }
+                                }
+                            }
+                    }
+                    double* pt = sp.part + (((size_t)s * sp.T_sim + j) * NWC + warp) * 5 * V;
+#pragma unroll
+                    for (int km = 0; km < 4; ++km) {
+                        if (km == 3 || sample) {
+                            double r[V];
+#pragma unroll
+                            for (int v = 0; v < V; ++v) r[v] = acc[km][v];
+                            warp_transpose_reduce<V>(r, lane);
+                            const int idx = reduce_index<V>(lane);
+                            if (idx < V) pt[km * V + idx] = r[0];
+                        }
+                    }
+                    const bool bad_any = __any_sync(0xffffffffu, bad);
+                    if (lane == 0) pt[4 * V] = bad_any ? 1.0 : 0.0;
+                }
+            }
+        } else {
         if (producer) {
             // ---- TMA producer: one elected lane streams the active tiles through the stages ----
             if (lane == 0) {
@@ -497,13 +700,13 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
             }
         }
 
+        }
+
         // ---- grid barrier + active count ------------------------------------------------------
         if (tid == 0) {
             int mine = 0;
-            for (int slot = 0; slot < ns; ++slot) {
-                const int s = s_lo + slot;
-                if ((long long)s * sp.T_sim >= t_lo && s_coef[slot].active) ++mine;   // owner CTA counts
-            }
+            for (int slot = 0; slot < ns; ++slot)
+                if (is_owner(slot) && s_coef[slot].active) ++mine;                       // owner CTA counts
             if (mine) atomicAdd(&sp.active[n % 3], mine);
         }
 #if PBE_TIMING
@@ -518,18 +721,29 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
         ++tc_steps;
 #endif
         const int still = *((volatile int*)&sp.active[n % 3]);
-        if (blockIdx.x == 0 && tid == 0) sp.active[(n + 2) % 3] = 0;      // read by all before barrier n
+        if (blockIdx.x == 0 && tid == 0) {
+            sp.active[(n + 2) % 3] = 0;                                   // read by all before barrier n
+            if (DYN) sp.tile_ctr[(n + 2) % 3] = 0u;                       // used by all before barrier n
+        }
         if (still == 0) break;
 
         // ---- scalar phase: one warp per simulation slot ----------------------------------------
+        if (DYN) {
+            if (warp < NWC)
+                for (int slot = 0; slot < ns; ++slot)
+                    if (s_coef[slot].active) cta_partials(slot, s_coef[slot].sample != 0);
+            __syncthreads();
+        }
+        if (DYN && warp < ns && !s_coef[warp].active) publish(warp, (unsigned)(n + 1));   // stays inactive
         if (warp < ns && s_coef[warp].active) {
-            const int slot = warp, s = s_lo + slot;
-            const bool owner = (long long)s * sp.T_sim >= t_lo;
+            const int slot = warp, s = sim_of_slot(slot);
+            const bool owner = is_owner(slot);
             SimPrimal W = s_sp[slot];
             SimTan T = s_st[slot][lane];
             const bool sample = s_coef[slot].sample != 0;
             double tot[4], totd[4], badf;
-            sim_totals(s, sample, tot, totd, badf);
+            if (DYN) cta_totals(slot, sample, tot, totd, badf);
+            else sim_totals(s, sample, tot, totd, badf);
             const D1 mu3n = mk(tot[3], totd[3]);
             const D1 c = mk(W.c, T.c), mu3p = mk(W.mu3p, T.mu3p);
             const D1 cn = c - kp.rho_kv * (mu3n - mu3p);
@@ -570,6 +784,7 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
                 set_inactive(slot);
                 if (owner && lane == 0) sp.final_buf[s] = src_sel ^ 1;   // state of this step is in dst
             }
+            publish(slot, (unsigned)(n + 1));
             __syncwarp();
             if (lane == 0) s_sp[slot] = W;
             s_st[slot][lane] = T;
@@ -591,8 +806,8 @@ __global__ void __launch_bounds__(STREAM_NT, StreamCfg<1 + P>::MINB) k_stream(co
 #endif
     // ---- epilogue: per-simulation status / loss / gradient (owner CTA) --------------------------
     if (warp < ns) {
-        const int slot = warp, s = s_lo + slot;
-        if ((long long)s * sp.T_sim >= t_lo) {
+        const int slot = warp, s = sim_of_slot(slot);
+        if (is_owner(slot)) {
             const SimPrimal W = s_sp[slot];
             const SimTan T = s_st[slot][lane];
             const bool ok = W.status == ST_OK;

@@ -63,7 +63,7 @@ struct pbe_ctx_s {
     // outputs
     DevBuf rec, trec, status, steps, loss, grad;
     // streaming-kernel scratch (allocated on first use)
-    DevBuf sbuf, spart, sbar, sfinal, snscale;
+    DevBuf sbuf, spart, sbar, sfinal, snscale, sdyn;
     // adjoint (NEXT-3) scratch: step trace, checkpoints, segment states, dL/dtheta
     DevBuf atr, ack, aseg, agrad;
     bool last_adjoint = false;
@@ -79,6 +79,7 @@ struct pbe_ctx_s {
     bool ws = true;          // env PBE_WS=0: lockstep k_resident instead of k_resident_ws for P >= 1
     int ws_variant = 0;      // env PBE_WS_VARIANT: k_resident_ws tuning variant (A/B only)
     bool ws_tail = true;     // env PBE_WS_TAIL=0: no half-lane CTAs for the last partial wave
+    bool stream_static = false;   // env PBE_STREAM_STATIC=1: k_stream with static tile ranges (A/B)
     bool temporal_block = true;  // NEXT-4 temporal blocking for uncapped-CFL steps mode in
                                  // k_stream (1.27x plain streaming on 64 x 1e6); env
                                  // PBE_TEMPORAL_BLOCK=0 selects plain streaming
@@ -185,12 +186,14 @@ const ResidentVariant* pick_cluster(int N, int P, int* cs) {
 // k_stream<P> variants: lanes per launch (the tangent lanes of a simulation are never split)
 struct StreamVariant {
     int P;
-    const void* fn;
+    const void* fn;          // k_stream<P, true>: dynamic tile schedule
+    const void* fn_static;   // k_stream<P, false>: static tile ranges (PBE_STREAM_STATIC=1, A/B)
     void (*load)(const double*, long long, int, int, double*, long long, unsigned long long*, int, int, double*,
                  double, double);
     void (*store)(const double*, const double*, const int*, int, int, long long, double*, double*);
 };
-#define SV(P) StreamVariant{P, (const void*)&pbe::k_stream<P>, &pbe::k_stream_load<1 + P>, &pbe::k_stream_store<1 + P>}
+#define SV(P) StreamVariant{P, (const void*)&pbe::k_stream<P, true>, (const void*)&pbe::k_stream<P, false>, \
+                            &pbe::k_stream_load<1 + P>, &pbe::k_stream_store<1 + P>}
 const StreamVariant kStream[] = {SV(0), SV(2), SV(4)};
 #undef SV
 const StreamVariant* pick_stream(int P) {
@@ -266,9 +269,11 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     const int TB = pbe::stream_tile(N, V);
     const int stages = V == 1 ? pbe::StreamCfg<1>::STAGES : pbe::StreamCfg<3>::STAGES;
     const size_t smem = (size_t)stages * V * (TB + 4) * sizeof(double);
-    CUDA_TRY(ctx, cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const bool dyn = !ctx->stream_static;
+    const void* fn = dyn ? sv.fn : sv.fn_static;
+    CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sv.fn, pbe::STREAM_NT, smem));
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, pbe::STREAM_NT, smem));
     if (per_sm < 1) return fail(ctx, PBE_ERR_CUDA, "k_stream does not fit on an SM (smem %zu)", smem);
     const int cap_sm = V == 1 && pbe::StreamCfg<1>::MINB > 2 ? pbe::StreamCfg<1>::MINB : 2;
     per_sm = per_sm > cap_sm ? cap_sm : per_sm;
@@ -276,7 +281,7 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     const int T_sim = (N + TB - 1) / TB;
     const long long n_tiles = (long long)S * T_sim;
     const long long chunk = (n_tiles + G - 1) / G;
-    if ((chunk + T_sim - 1) / T_sim + 1 > pbe::STREAM_MAXS)
+    if (dyn ? (S + G - 1) / G > pbe::STREAM_MAXS : (chunk + T_sim - 1) / T_sim + 1 > pbe::STREAM_MAXS)
         return fail(ctx, PBE_ERR_ARG, "too many simulations per CTA for the streaming kernel (S = %d, N = %d)", S, N);
 
     const size_t buf_el = (size_t)S * V * pitch;
@@ -285,12 +290,16 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     CUDA_TRY(ctx, ctx->sbar.ensure(8 * sizeof(unsigned)));
     CUDA_TRY(ctx, ctx->sfinal.ensure((size_t)S * sizeof(int)));
     CUDA_TRY(ctx, ctx->snscale.ensure((size_t)S * sizeof(unsigned long long)));
+    // dynamic schedule: [4] tile counters, [S] coefficient steps, then [S] coefficients (16-B aligned)
+    CUDA_TRY(ctx, ctx->sdyn.ensure((4 + (size_t)S) * sizeof(unsigned) + 16 + (size_t)S * 16 * sizeof(double)));
     double* b0 = ctx->sbuf.as<double>();
     double* b1 = b0 + buf_el;
     // ghosts and padding must be zero in both buffers (only interior bins are ever written)
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbuf.p, 0, 2 * buf_el * sizeof(double), st));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->sbar.p, 0, 8 * sizeof(unsigned), st));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->snscale.p, 0, (size_t)S * sizeof(unsigned long long), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sdyn.p, 0, 4 * sizeof(unsigned), st));                  // tile counters
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sdyn.as<unsigned>() + 4, 0xff, (size_t)S * sizeof(unsigned), st));  // no step yet
     sv.load<<<dim3(T_sim, S), 256, 0, st>>>(n0, n0_stride, N, S, b0, pitch, ctx->snscale.as<unsigned long long>(),
                                             TB, T_sim, ctx->spart.as<double>(), kp.L_lo, kp.dL);
     CUDA_TRY(ctx, cudaGetLastError());
@@ -304,9 +313,12 @@ static pbe_status launch_stream(pbe_ctx ctx, const StreamVariant& sv, KParams kp
     sp.active = reinterpret_cast<int*>(ctx->sbar.as<unsigned>() + 4);
     sp.final_buf = ctx->sfinal.as<int>();
     sp.nscale_bits = ctx->snscale.as<unsigned long long>();
+    sp.tile_ctr = ctx->sdyn.as<unsigned>();
+    sp.coef_step = ctx->sdyn.as<unsigned>() + 4;
+    sp.coef = reinterpret_cast<char*>(ctx->sdyn.p) + (((4 + (size_t)S) * sizeof(unsigned) + 15) / 16) * 16;
     void* args[] = {&sp};
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    CUDA_TRY(ctx, cudaLaunchCooperativeKernel(sv.fn, dim3(G), dim3(pbe::STREAM_NT), args, smem, st));
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(pbe::STREAM_NT), args, smem, st));
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
     int launches = 2;
     if (kp.n_final || kp.ndot_final) {
@@ -687,6 +699,7 @@ pbe_status pbe_create(const pbe_config* cfg, int device, pbe_ctx* out) {
     if (const char* e = getenv("PBE_WS")) ctx->ws = atoi(e) != 0;
     if (const char* e = getenv("PBE_WS_VARIANT")) ctx->ws_variant = atoi(e);
     if (const char* e = getenv("PBE_WS_TAIL")) ctx->ws_tail = atoi(e) != 0;
+    if (const char* e = getenv("PBE_STREAM_STATIC")) ctx->stream_static = atoi(e) != 0;
     if (const char* e = getenv("PBE_TEMPORAL_BLOCK")) ctx->temporal_block = atoi(e) != 0;
     if (const char* e = getenv("PBE_2D_UNFUSED")) ctx->unfused_2d = atoi(e) != 0;
     ctx->device = device;
@@ -718,7 +731,7 @@ void pbe_destroy(pbe_ctx ctx) {
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->theta, &ctx->sol, &ctx->knot_t, &ctx->knot_T, &ctx->seed, &ctx->c0, &ctx->tsamp,
                       &ctx->target, &ctx->n0_staged, &ctx->rec, &ctx->trec, &ctx->status, &ctx->steps,
-                      &ctx->loss, &ctx->grad, &ctx->sbuf, &ctx->spart, &ctx->sbar, &ctx->sfinal, &ctx->snscale, &ctx->atr, &ctx->ack, &ctx->aseg, &ctx->agrad})
+                      &ctx->loss, &ctx->grad, &ctx->sbuf, &ctx->spart, &ctx->sbar, &ctx->sfinal, &ctx->snscale, &ctx->sdyn, &ctx->atr, &ctx->ack, &ctx->aseg, &ctx->agrad})
         b->release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);

@@ -37,6 +37,8 @@
 //  double-buffered by step parity; warp 0 runs the scalar phases (two barriers per step).
 // =====================================================================================
 #pragma once
+#include <type_traits>
+
 #include "pbe_device.cuh"
 
 namespace pbe {
@@ -119,6 +121,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     double* s_trs = sm + 4 * NP + (ap.seg_smem ? (size_t)(Kseg + 1) * N : 0);
     __shared__ double s_red[32][4];
     __shared__ double s_sc[12];
+    __shared__ double s_pp[32][2];                 // long polynomial: per-warp (G, dG/dx) partials
+    __shared__ double s_cm[2];                     // warp 0's c, mu3p (read by every warp)
     __shared__ int s_go, s_sample, s_bad, s_ok;
     __shared__ long long s_nsteps;
     enum { SC_C = 0, SC_KAP2, SC_BETA2, SC_LM, SC_L0, SC_L1, SC_LG, SC_S, SC_T, SC_CLIP };
@@ -163,22 +167,47 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         return t;
     };
     // forward update nb[q] -> nb[q^1] (eq-highRes_growth, flux form; clip marks as -0.0)
+    // limited half slope of kind LIMT (0 upwind, 1 van Leer branch-free, 2 minmod/superbee/MC):
+    // the sweep direction and the limiter are resolved once per step, not per face (a branch per
+    // face makes every face its own basic block and serialises their latency chains)
+    auto half_slope = [&](auto limc, double a, double b, double& h, double& qa, double& qb)
+        __attribute__((always_inline)) {
+        constexpr int LIMT = decltype(limc)::value;
+        h = qa = qb = 0.0;
+        if (LIMT == 1) psi_half_d_bf(a, b, h, qa, qb);
+        else if (LIMT == 2) psi_half_other(lim, a, b, h, qa, qb);
+    };
+    auto with_kind = [&](double C, auto&& body) __attribute__((always_inline)) {
+        const int lk = lim == LIM_VANLEER ? 1 : (lim == LIM_UPWIND ? 0 : 2);
+        if (C >= 0.0) {
+            if (lk == 1) return body(std::false_type{}, std::integral_constant<int, 1>{});
+            if (lk == 0) return body(std::false_type{}, std::integral_constant<int, 0>{});
+            return body(std::false_type{}, std::integral_constant<int, 2>{});
+        }
+        if (lk == 1) return body(std::true_type{}, std::integral_constant<int, 1>{});
+        if (lk == 0) return body(std::true_type{}, std::integral_constant<int, 0>{});
+        return body(std::true_type{}, std::integral_constant<int, 2>{});
+    };
     auto update = [&](int q, double C, double kap2, double clip) -> bool {
         const double* in = nb + q * NP + i0;                       // in[j] = bin i0 - 2 + j
         double* out = nb + (q ^ 1) * NP + i0 + 2;
         double w[K + 4], F[K + 1];
 #pragma unroll
         for (int j = 0; j < K + 4; ++j) w[j] = in[j];
+        with_kind(C, [&](auto negc, auto limc) {
+            constexpr bool NEG = decltype(negc)::value;
 #pragma unroll
-        for (int f = 0; f <= K; ++f) {                             // face between bins i0+f-1 | i0+f
-            if (C >= 0.0) {
-                const double h = psi_half(lim, w[f + 1] - w[f], w[f + 2] - w[f + 1]);
-                F[f] = fma(C, w[f + 1], kap2 * h);
-            } else {
-                const double h = psi_half(lim, w[f + 3] - w[f + 2], w[f + 2] - w[f + 1]);
-                F[f] = fma(C, w[f + 2], kap2 * h);
+            for (int f = 0; f <= K; ++f) {                         // face between bins i0+f-1 | i0+f
+                double h, qa, qb;
+                if (!NEG) {
+                    half_slope(limc, w[f + 1] - w[f], w[f + 2] - w[f + 1], h, qa, qb);
+                    F[f] = fma(C, w[f + 1], kap2 * h);
+                } else {
+                    half_slope(limc, w[f + 3] - w[f + 2], w[f + 2] - w[f + 1], h, qa, qb);
+                    F[f] = fma(C, w[f + 2], kap2 * h);
+                }
             }
-        }
+        });
         bool bad = false;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -208,13 +237,51 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     // kinetics of the step from (c, t) + its linearisation (lane 0: dc, lane 1: dt, lane 2: dG)
     const KinCache KC = kin_cache(kp, KL, kT);           // constant: theta, solubility, knots
     double tn_c = kp.t_samples[0];                         // t_samples[m], read once per sample
+    // long polynomial at constant T (NEXT-3's 1000-coefficient regime): the terms are split over
+    // EVERY thread of the CTA (the other warps would idle at the barrier while warp 0 runs the
+    // kinetics): thread t sums terms [t m, t m + m) by Horner with d/dx, scaled by x^(t m + 1);
+    // warp butterflies, then warp 0 adds the warp partials in warp order.  Step 0 uses the
+    // warp-cooperative form.
+    const bool poly_blk = kp.law == LAW_POLY && kp.n_params > MAXTH && KC.const_T;
+    bool use_blk = false;                                  // warp 0: the partials of this step are ready
+    auto poly_partials = [&](double Sv) {                  // every thread, after the step's barrier
+        double tt = 0.0, dtt = 0.0;
+        if (Sv > 1.0) {
+            const double x = Sv - 1.0;
+            const int mm = (kp.n_params + NT - 1) / NT, j0 = tid * mm;
+            const double* a = kp.theta + (size_t)s * kp.n_params;
+            double qv = 0.0, dq = 0.0;
+            for (int i = mm - 1; i >= 0; --i) {
+                const int j = j0 + i;
+                const double aj = j < kp.n_params ? __ldg(a + j) : 0.0;
+                dq = fma(dq, x, qv);
+                qv = fma(qv, x, aj);
+            }
+            const double xl = ipow(x, j0);
+            tt = xl * x * qv;
+            dtt = xl * fma((double)(j0 + 1), qv, x * dq);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            tt += __shfl_xor_sync(0xffffffffu, tt, off);
+            dtt += __shfl_xor_sync(0xffffffffu, dtt, off);
+        }
+        if (lane == 0) { s_pp[warp][0] = tt; s_pp[warp][1] = dtt; }
+    };
     auto kinetics = [&](long long k) -> bool {
         const D1 cD = mk(c, lane == 0 ? 1.0 : 0.0), tD = mk(t, lane == 1 ? 1.0 : 0.0);
         D1 T;
         const D1 S = supersaturation(kp, KL, kT, KC, tD, cD, T);
-        D1 G = (kp.law == LAW_POLY && kp.n_params > MAXTH)
-                   ? poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S)   // warp-cooperative
-                   : growth_rate(kp, KL, S, T);
+        D1 G;
+        if (use_blk) {                                     // block partials of this S (same value)
+            double tt = 0.0, dtt = 0.0;
+            for (int w = 0; w < NW; ++w) { tt += s_pp[w][0]; dtt += s_pp[w][1]; }
+            G = S.v > 1.0 ? D1{tt, dtt * S.d} : mk(0.0);
+        } else {
+            G = (kp.law == LAW_POLY && kp.n_params > MAXTH)
+                    ? poly_long_warp(kp.theta + (size_t)s * kp.n_params, kp.n_params, S)   // warp-cooperative
+                    : growth_rate(kp, KL, S, T);
+        }
         if (lane == 2) G = mk(G.v, 1.0);
         const double tn = tn_c;
         const StepScalars sc = time_step(kp, G, tD, tn, false);
@@ -258,6 +325,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             s_go = go;
             s_sample = go && landing;
             s_sc[SC_CLIP] = 1e-12 * nmax;
+            s_cm[0] = c; s_cm[1] = mu3p;
         }
     }
     __syncthreads();
@@ -276,10 +344,17 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         if (update(q, s_sc[SC_C], s_sc[SC_KAP2], clip)) s_bad = 1;
         moment_partials(q ^ 1, s_sample != 0);
         __syncthreads();
+        if (poly_blk) {
+            // every warp: c^{k+1} and S of the next step exactly as warp 0 forms them below
+            const double cn = __dsub_rn(s_cm[0], __dmul_rn(rho, __dsub_rn(block_total(3), s_cm[1])));
+            poly_partials(__dmul_rn(cn, KC.ics.v));
+            __syncthreads();
+            use_blk = true;
+        }
         if (warp == 0) {
             const bool sample = s_sample != 0;
             const double mu3 = block_total(3);
-            const double cn = c - rho * (mu3 - mu3p);                     // eq-discrete_mass_balance
+            const double cn = __dsub_rn(c, __dmul_rn(rho, __dsub_rn(mu3, mu3p)));   // eq-discrete_mass_balance
             bool go = true;
             if (s_bad) { status = ST_NEG; go = false; }
             else if (cn < 0.0) { status = ST_INFEAS; go = false; }
@@ -307,7 +382,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                 else if (nstep >= kp.max_steps) { status = ST_MAXSTEPS; go = false; }
                 else go = kinetics(k + 1);
             }
-            if (lane == 0) { s_go = go; s_sample = go && landing; s_nsteps = nstep; }
+            if (lane == 0) { s_go = go; s_sample = go && landing; s_nsteps = nstep; s_cm[0] = c; s_cm[1] = mu3p; }
         }
         __syncthreads();
         q ^= 1;
@@ -337,8 +412,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         if (kp.law == LAW_POLY) {                  // dG/da_j = (S-1)^(j+1): x^(tid+1) x (x^NT)^g
             if (!(S > 1.0)) return;
             const double X = S - 1.0;
-            double xp = pow(X, (double)(tid + 1));
-            const double xs = pow(X, (double)NT);
+            double xp = ipow(X, tid + 1);
+            const double xs = ipow(X, NT);
 #pragma unroll
             for (int g = 0; g < ADJ_GMAX; ++g) {
                 if (tid + g * NT < kp.n_params) gacc[g] = fma(lamG, xp, gacc[g]);
@@ -425,30 +500,29 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             // face partials (as k_resident's tangent lanes): faces f = i0 - 1 + e, e = 0..K+2
             double Lf[K + 3], whi[K + 3], wmid[K + 3], wlo[K + 3];
             double lamC = 0.0;
+            with_kind(C, [&](auto negc, auto limc) {
+                constexpr bool NEG = decltype(negc)::value;
 #pragma unroll
-            for (int e = 0; e < K + 3; ++e) {
-                const int f = i0 - 1 + e;                                // face between bins f-1 | f
-                // window index of bin f: f - (i0 - 2) = e + 1
-                double a, b, nup;
-                if (C >= 0.0) {
-                    if (e < 1) { Lf[e] = 0.0; whi[e] = wmid[e] = wlo[e] = 0.0; continue; }
-                    a = w[e] - w[e - 1]; b = w[e + 1] - w[e]; nup = w[e];
-                } else {
-                    if (e > K + 1) { Lf[e] = 0.0; whi[e] = wmid[e] = wlo[e] = 0.0; continue; }
-                    a = w[e + 2] - w[e + 1]; b = w[e + 1] - w[e]; nup = w[e + 1];
+                for (int e = 0; e < K + 3; ++e) {
+                    const int f = i0 - 1 + e;                            // face between bins f-1 | f
+                    // window index of bin f: f - (i0 - 2) = e + 1
+                    if ((!NEG && e < 1) || (NEG && e > K + 1)) { Lf[e] = 0.0; whi[e] = wmid[e] = wlo[e] = 0.0; continue; }
+                    const double a = NEG ? w[e + 2] - w[e + 1] : w[e] - w[e - 1];
+                    const double b = w[e + 1] - w[e];
+                    const double nup = NEG ? w[e + 1] : w[e];
+                    double h, qa, qb;
+                    half_slope(limc, a, b, h, qa, qb);
+                    const double pak = kap2 * qa, pbk = kap2 * qb;
+                    if (!NEG) { whi[e] = pbk; wmid[e] = C + (pak - pbk); wlo[e] = -pak; }
+                    else      { whi[e] = pak; wmid[e] = C - (pak - pbk); wlo[e] = -pbk; }
+                    Lf[e] = lam[e + 1] - lam[e];                         // lambda_f - lambda_{f-1}
+                    // faces [i0, i0+K) of a thread holding real bins, plus the outflow face N for the
+                    // thread whose last bin is N-1 (a thread starting at i0 = N owns none: when N % K == 0
+                    // it would otherwise count face N a second time)
+                    const bool owned = i0 < N && ((f >= i0 && f < i0 + K && f <= N) || (f == N && i0 + K == N));
+                    if (owned) lamC = fma(Lf[e], fma(beta2, h, nup), lamC); // dF/dC = n_up + beta psi
                 }
-                double h = 0.0, qa = 0.0, qb = 0.0;
-                psi_half_dl(lim, a, b, h, qa, qb);
-                const double pak = kap2 * qa, pbk = kap2 * qb;
-                if (C >= 0.0) { whi[e] = pbk; wmid[e] = C + (pak - pbk); wlo[e] = -pak; }
-                else          { whi[e] = pak; wmid[e] = C - (pak - pbk); wlo[e] = -pbk; }
-                Lf[e] = lam[e + 1] - lam[e];                             // lambda_f - lambda_{f-1}
-                // faces [i0, i0+K) of a thread holding real bins, plus the outflow face N for the
-                // thread whose last bin is N-1 (a thread starting at i0 = N owns none: when N % K == 0
-                // it would otherwise count face N a second time)
-                const bool owned = i0 < N && ((f >= i0 && f < i0 + K && f <= N) || (f == N && i0 + K == N));
-                if (owned) lamC = fma(Lf[e], fma(beta2, h, nup), lamC); // dF/dC = n_up + beta psi
-            }
+            });
             double* lout = lb + (ql ^ 1) * NP + i0 + 2;
 #pragma unroll
             for (int kq = 0; kq < K; ++kq) {

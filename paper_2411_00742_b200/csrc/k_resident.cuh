@@ -191,7 +191,7 @@ __device__ __forceinline__ D1 poly_long_warp_seeded(const double* __restrict__ a
         for (int p = 0; p < PP; ++p)
             sp[p] = fma(sp[p], x, (on && p < nl) ? __ldg(seed + (size_t)(lane0 + p) * nsd + j) : 0.0);
     }
-    const double xl = pow(x, (double)j0), xl1 = xl * x;   // x^(l m), x^(l m + 1)
+    const double xl = ipow(x, j0), xl1 = xl * x;          // x^(l m), x^(l m + 1)
     double t = xl1 * q;
     double dt = xl * fma((double)(j0 + 1), q, x * dq);
 #pragma unroll

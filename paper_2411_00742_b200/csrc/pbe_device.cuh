@@ -189,6 +189,18 @@ __device__ __forceinline__ D1 growth_rate(const KParams& kp, const LD& L, D1 S, 
     return mk(0.0);
 }
 
+// x^e for an integer e >= 0 by binary exponentiation (<= 2 log2(e) multiplications instead of
+// pow()'s exp/log: the long-polynomial chunk offsets and the adjoint's d G / d a_j = x^(j+1)).
+__device__ __forceinline__ double ipow(double x, int e) {
+    double r = 1.0, b = x;
+    while (e > 0) {
+        if (e & 1) r *= b;
+        e >>= 1;
+        if (e) b *= b;
+    }
+    return r;
+}
+
 // Long polynomial growth law (n > MAXTH terms; NEXT-3's 1000-coefficient regime) evaluated
 // cooperatively by the 32 lanes of a warp, for lanes WITHOUT parameter seeds: lane l sums the
 // terms j in [l m, l m + m), m = ceil(n/32), by Horner (value and d/dx), scales by x^(l m + 1),
@@ -208,7 +220,7 @@ __device__ __forceinline__ D1 poly_long_warp(const double* __restrict__ a, int n
         dq = fma(dq, x, q);
         q = fma(q, x, aj);
     }
-    const double xl = pow(x, (double)j0);             // x^(l m)
+    const double xl = ipow(x, j0);                    // x^(l m)
     double t = xl * x * q;                             // x^(l m + 1) q(x)
     double dt = xl * fma((double)(j0 + 1), q, x * dq); // (l m + 1) x^(l m) q + x^(l m + 1) q'
 #pragma unroll

@@ -49,7 +49,7 @@ __device__ unsigned long long g_phase_cycles[12];   // sweep, moments+publish, b
 // Smem halo: s_halo[(side * V + v) * HS + t + 1], HS = NT + 2, side 0/1 = bins 0/1 of
 // thread t, side 2/3 = bins K-2/K-1 (transposed so a warp's accesses are consecutive).
 // Columns 0 and NT + 1 stay zero: the ghost cells n_{-2} = n_{-1} = n_N = n_{N+1} = 0.
-template <int P, int K, bool NEG, bool GEN, class CdT>
+template <int P, int K, bool NEG, int LK, class CdT>   // LK: 0 upwind, 1 van Leer, 2 minmod/superbee/MC
 __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* __restrict__ s_halo,
                                            int NT, int tid, double C, double kap, double beta,
                                            const CdT& Cd, int lim, int i0, int N,
@@ -84,8 +84,8 @@ __device__ __forceinline__ bool sweep_bins(double (&x)[1 + P][K], const double* 
         const int ja = NEG ? f + 1 : f - 1;
         const double a = X(0, ja) - X(0, ja - 1), b = X(0, f) - X(0, f - 1);
         double h = 0.0, qa = 0.0, qb = 0.0;          // psi = 2h, d psi/da = 2qa, d psi/db = 2qb
-        if (GEN) psi_half_other(lim, a, b, h, qa, qb);        // minmod / superbee / MC (NEXT-4)
-        else if (lim == LIM_VANLEER) psi_half_d(a, b, h, qa, qb);
+        if (LK == 2) psi_half_other(lim, a, b, h, qa, qb);     // minmod / superbee / MC (NEXT-4)
+        else if (LK == 1) psi_half_d_bf(a, b, h, qa, qb);      // no branch: faces overlap
         const double nup = X(0, u);
         FaceP r;
         r.F = fma(C, nup, kap2 * h);                   // C n_up + kap psi
@@ -530,24 +530,30 @@ __global__ void __launch_bounds__(MAXT, MINB) k_resident(const KParams kp) {
             double Cd[PP];
 #pragma unroll
             for (int p = 0; p < PP; ++p) Cd[p] = (p < P) ? __shfl_sync(0xffffffffu, Cd_l, p) : 0.0;
-            if (!gen) {
-                if (C >= 0.0) bad = sweep_bins<P, K, false, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
-                else          bad = sweep_bins<P, K, true, false>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+            if (vl == LIM_VANLEER) {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, 1>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, 1>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+            } else if (!gen) {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, 0>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, 0>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
             } else {
-                if (C >= 0.0) bad = sweep_bins<P, K, false, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
-                else          bad = sweep_bins<P, K, true, true>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+                if (C >= 0.0) bad = sweep_bins<P, K, false, 2>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, 2>(x, hin, NT, tid, C, kap, beta, Cd, vl, i0, N, clip_thr);
             }
         } else {
             // 2 CTAs/SM (<= 128 registers): lane tangents of C re-read from this warp's smem slot
             volatile double* cdw = s_cdw + warp * PP;
             if (lane < PP) cdw[lane] = Cd_l;
             __syncwarp();
-            if (!gen) {
-                if (C >= 0.0) bad = sweep_bins<P, K, false, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
-                else          bad = sweep_bins<P, K, true, false>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+            if (vl == LIM_VANLEER) {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, 1>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, 1>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+            } else if (!gen) {
+                if (C >= 0.0) bad = sweep_bins<P, K, false, 0>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, 0>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
             } else {
-                if (C >= 0.0) bad = sweep_bins<P, K, false, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
-                else          bad = sweep_bins<P, K, true, true>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+                if (C >= 0.0) bad = sweep_bins<P, K, false, 2>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
+                else          bad = sweep_bins<P, K, true, 2>(x, hin, NT, tid, C, kap, beta, cdw, vl, i0, N, clip_thr);
             }
         }
         PBE_TSTAMP(tc1);

@@ -169,7 +169,7 @@ __device__ __forceinline__ void stream_bins(const double* __restrict__ sb, int R
         if (LK == 2) psi_half_dl(lim, a, b, h, qa, qb);
         else if (LK == 1) {
             if (P == 0) h = psi_half_vl_sf(a, b);            // primal only: select-free
-            else psi_half_d(a, b, h, qa, qb);
+            else psi_half_d_bf(a, b, h, qa, qb);
         }
         const double nup = x[0][u];
         F[f - 2] = fma(C, nup, kap2 * h);

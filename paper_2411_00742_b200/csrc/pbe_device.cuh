@@ -406,7 +406,7 @@ __device__ __forceinline__ double psi_half(int lim, double a, double b) {
 }
 // h and the half partials for the tangent / adjoint lanes, any limiter.
 __device__ __forceinline__ void psi_half_dl(int lim, double a, double b, double& h, double& qa, double& qb) {
-    if (lim == LIM_VANLEER) { psi_half_d(a, b, h, qa, qb); return; }
+    if (lim == LIM_VANLEER) { psi_half_d_bf(a, b, h, qa, qb); return; }
     if (lim == LIM_UPWIND) { h = qa = qb = 0.0; return; }
     psi_half_other(lim, a, b, h, qa, qb);
 }

@@ -71,7 +71,23 @@ struct AdjParams {
     long long n_ck;       // checkpoint slots per simulation
     int Kseg;
     int seg_smem;         // 1: the segment states live in shared memory (seg unused)
+    int traj;             // 1: every state n^0..n^K is kept (ck holds K + 1 rows): no re-march, the
+                          //    reverse pass prefetches n^{k-1} with cp.async while it works on k
 };
+
+// 16-byte global -> shared copy that bypasses registers (LDGSTS), and its completion wait
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 // dG/dtheta_j at (S, T) in closed form (the parameters enter the laws of growth_rate as
 // below; dpow(x, y) = exp(y log x) there).
@@ -111,14 +127,26 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const double rho = kp.rho_kv;
     const int Kseg = ap.Kseg;
     double* trs = ap.tr + (size_t)s * kp.max_steps * ADJ_TR;
-    double* cks = ap.ck + (size_t)s * ap.n_ck * N;
-    extern __shared__ double sm[];
+    const int CP = ap.traj ? (N + 1) & ~1 : N;          // checkpoint row pitch (16-B rows for cp.async)
+    double* cks = ap.ck + (size_t)s * ap.n_ck * CP;
+    extern __shared__ __align__(16) double sm[];
     double* nb = sm;                      // [2][NP] states, bin i at [i + 2]
     double* lb = sm + 2 * NP;             // [2][NP] adjoints
-    // segment states n^{k0..k1}: shared memory when they fit (host decides), else global
-    double* sgs = ap.seg_smem ? sm + 4 * NP : ap.seg + (size_t)s * (Kseg + 1) * N;
+    // segment states n^{k0..k1}: shared memory when they fit (host decides), else global;
+    // trajectory mode: a ring of 3 states (n^{k+1}, n^k and n^{k-1} in flight), 16-byte rows
+    const int NR = (N + 1) & ~1;
+    double* sgs = (ap.seg_smem || ap.traj) ? sm + 4 * NP : ap.seg + (size_t)s * (Kseg + 1) * N;
     // the segment's trace rows, staged in shared memory at every segment start
-    double* s_trs = sm + 4 * NP + (ap.seg_smem ? (size_t)(Kseg + 1) * N : 0);
+    double* s_trs = sm + 4 * NP + (ap.traj ? (size_t)3 * NR : (ap.seg_smem ? (size_t)(Kseg + 1) * N : 0));
+    // trajectory mode: state k -> ring slot k % 3, copied by this thread's 16-byte chunks
+    auto fetch_state = [&](long long k) {
+        const double* src = cks + (size_t)k * CP;
+        double* dst = sgs + (size_t)(k % 3) * NR;
+        for (int j = 2 * tid; j < N; j += 2 * NT) {
+            if (j + 1 < N) cp_async16(dst + j, src + j);
+            else cp_async8(dst + j, src + j);
+        }
+    };
     __shared__ double s_red[32][4];
     __shared__ double s_sc[12];
     __shared__ double s_pp[32][2];                 // long polynomial: per-warp (G, dG/dx) partials
@@ -336,8 +364,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     long long k = 0;
     PBE_ATS(tf0);
     while (s_go) {
-        if (k % Kseg == 0) {
-            double* ckp = cks + (size_t)(k / Kseg) * N;
+        if (ap.traj || k % Kseg == 0) {
+            double* ckp = cks + (size_t)(ap.traj ? k : k / Kseg) * CP;
 #pragma unroll
             for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + i0 + j + 2];
         }
@@ -387,6 +415,11 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         __syncthreads();
         q ^= 1;
         ++k;
+    }
+    if (ap.traj) {                                         // the final state n^K closes the trajectory
+        double* ckp = cks + (size_t)k * CP;
+#pragma unroll
+        for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + i0 + j + 2];
     }
     PBE_ATS(tf1);
     PBE_ATA(0, tf0, tf1);
@@ -439,6 +472,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     bool have_lg = false;
     double lg_prev = 0.0, S_prev = 0.0, T_prev = 0.0;
     const long long nseg = (Ktot + Kseg - 1) / Kseg;
+    if (ap.traj && Ktot > 0) {                             // n^K and n^{K-1} before the first step
+        __syncthreads();                                   // the final state's global stores are done
+        __threadfence_block();
+        fetch_state(Ktot);
+        fetch_state(Ktot - 1);
+        cp_async_commit_wait_all();
+    }
     for (long long sg = nseg - 1; sg >= 0; --sg) {
         const long long k0 = sg * Kseg, k1 = min(k0 + (long long)Kseg, Ktot);
         // stage the segment's trace rows (read by every step below)
@@ -448,7 +488,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         __syncthreads();
         // re-march the segment from its checkpoint (C^k from the trace): states n^{k0..k1}
         PBE_ATS(tr0);
-        {
+        if (!ap.traj) {
             const double* ckp = cks + (size_t)sg * N;
 #pragma unroll
             for (int j = 0; j < K; ++j) if (i0 + j < N) nb[i0 + j + 2] = ckp[i0 + j];
@@ -475,11 +515,12 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             PBE_ATS(tb0);
             // ---- vector phase: lambda^{kk+1} (+ mass-balance and sample terms, clip marks) ->
             //      lambda^kk, partial lambda_C -------------------------------------------------
+            if (ap.traj && kk >= 1) { fetch_state(kk - 1); cp_async_commit(); }   // lands while we work
             if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
             const double C = s_sc[SC_C], kap2 = s_sc[SC_KAP2], beta2 = s_sc[SC_BETA2];
             const double lm = s_sc[SC_LM], l0 = s_sc[SC_L0], l1 = s_sc[SC_L1];
-            const double* nk = sgs + (size_t)(kk - k0) * N;            // n^kk
-            const double* nk1 = nk + N;                                 // n^{kk+1}
+            const double* nk = ap.traj ? sgs + (size_t)(kk % 3) * NR : sgs + (size_t)(kk - k0) * N;   // n^kk
+            const double* nk1 = ap.traj ? sgs + (size_t)((kk + 1) % 3) * NR : nk + N;                // n^{kk+1}
             const double* lin = lb + ql * NP + i0;                      // lin[j] = raw lambda of bin i0-2+j
             double w[K + 4], lam[K + 4];
 #pragma unroll
@@ -552,6 +593,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                 if (lane == 0) { s_sc[SC_LG] = lG; s_sc[SC_S] = r[TR_S]; s_sc[SC_T] = r[TR_T]; }
                 if (kk > k0) pre_step(kk - 1);
             }
+            if (ap.traj) asm volatile("cp.async.wait_group 0;" ::: "memory");   // n^{kk-1}: this thread's part
             __syncthreads();
             lg_prev = s_sc[SC_LG]; S_prev = s_sc[SC_S]; T_prev = s_sc[SC_T];
             have_lg = true;

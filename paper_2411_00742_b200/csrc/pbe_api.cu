@@ -1021,9 +1021,19 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     // its states n^{k0..k1} live there too when they fit (else in a global buffer)
     const size_t smem_cap = 220 * 1024, row = (size_t)N * sizeof(double), trow = pbe::ADJ_TR * sizeof(double);
     int Kseg = checkpoint_every;
+    // checkpoint_every = 0 (auto): keep the whole trajectory in HBM when it takes <= 16 GB (C5-size
+    // NEXT-3: 9 x 12,001 x 2000 doubles = 1.7 GB) -- no re-march in the reverse pass; else O(sqrt)
+    const int NRr = (N + 1) & ~1;
+    const bool traj = checkpoint_every == 0 &&
+                      (double)n_sims * (ms + 1) * N * sizeof(double) <= 16.0 * (1ull << 30) &&
+                      smem + (size_t)3 * NRr * sizeof(double) + 64 * (size_t)pbe::ADJ_TR * sizeof(double) <= 220 * 1024 &&
+                      !getenv("PBE_ADJ_RECOMPUTE");
     if (Kseg == 0) Kseg = std::max(8, (int)std::ceil(std::sqrt((double)ms)));       // O(sqrt) memory
     int seg_smem = 0;
-    {
+    if (traj) {
+        Kseg = 64;                                        // trace rows staged per segment
+        smem += (size_t)3 * NRr * sizeof(double);
+    } else {
         // largest K' <= Kseg with the states in shared memory; take it when K' >= min(Kseg, 4)
         long long kfit = ((long long)smem_cap - (long long)smem - (long long)row) / (long long)(row + trow);
         if (kfit >= std::min(Kseg, 4)) { Kseg = (int)std::min<long long>(Kseg, kfit); seg_smem = 1; }
@@ -1034,10 +1044,10 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
         }
     }
     smem += (size_t)Kseg * trow + (seg_smem ? (size_t)(Kseg + 1) * row : 0);
-    const long long n_ck = (ms + Kseg - 1) / Kseg;
+    const long long n_ck = traj ? ms + 1 : (ms + Kseg - 1) / Kseg;
     const size_t tr_b = (size_t)n_sims * ms * pbe::ADJ_TR * sizeof(double);
-    const size_t ck_b = (size_t)n_sims * n_ck * N * sizeof(double);
-    const size_t sg_b = seg_smem ? sizeof(double) : (size_t)n_sims * (Kseg + 1) * N * sizeof(double);
+    const size_t ck_b = (size_t)n_sims * n_ck * (traj ? NRr : N) * sizeof(double);
+    const size_t sg_b = (seg_smem || traj) ? sizeof(double) : (size_t)n_sims * (Kseg + 1) * N * sizeof(double);
     if ((double)tr_b + ck_b + sg_b > 64.0 * (1ull << 30))
         return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: trace + checkpoints need %.1f GB (> 64 GB): lower max_steps or n_sims",
                     ((double)tr_b + ck_b + sg_b) / (1ull << 30));
@@ -1056,7 +1066,7 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     ap.kp = make_kparams(ctx, n_sims, n0_dev, n0_stride, target, nullptr, nullptr, 1);
     ap.kp.P = 0;
     ap.ck = ctx->ack.as<double>(); ap.seg = ctx->aseg.as<double>(); ap.tr = ctx->atr.as<double>();
-    ap.gtheta = ctx->agrad.as<double>(); ap.n_ck = n_ck; ap.Kseg = Kseg; ap.seg_smem = seg_smem;
+    ap.gtheta = ctx->agrad.as<double>(); ap.n_ck = n_ck; ap.Kseg = Kseg; ap.seg_smem = seg_smem; ap.traj = traj;
     CUDA_TRY(ctx, cudaFuncSetAttribute(av->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ctx->info = pbe_run_info{};
     void* args[] = {&ap};

@@ -131,6 +131,18 @@ def test_adjoint_checkpoint_interval_is_bitwise_neutral():
     assert np.array_equal(g1["grad"], g7["grad"]) and np.array_equal(g1["grad"], g0["grad"])
 
 
+@pytest.mark.parametrize("N", [97, 128])
+def test_adjoint_trajectory_mode_matches_recompute_mode(N, monkeypatch):
+    """checkpoint_every=0 keeps every state in HBM (cp.async ring, no re-march); the O(sqrt K)
+    checkpoint mode re-marches each segment.  Same arithmetic -> bitwise equal (odd N: the
+    8-byte tail copy of the ring prefetch)."""
+    w = small_ensemble(n_sims=3, N=N, M=10, t_max=20.0)
+    g0, _, info0 = gpu_adjoint(w, checkpoint_every=0)
+    monkeypatch.setenv("PBE_ADJ_RECOMPUTE", "1")
+    g1, _, _ = gpu_adjoint(w, checkpoint_every=0)
+    assert np.array_equal(g0["grad"], g1["grad"]) and np.array_equal(g0["loss"], g1["loss"])
+
+
 def test_adjoint_agrees_with_gpu_tangents():
     """The two GPU differentiation modes (k_resident tangent lanes, k_adjoint) agree."""
     import paper_2411_00742_b200 as pb

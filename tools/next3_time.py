@@ -42,6 +42,19 @@ def main():
     res.update(adjoint_ms=1e3 * min(times), adjoint_kernel_ms=ctx.last_run_info()["main_ms"],
                steps=int(rec["steps"].max()), loss=float(g["loss"].sum()))
     ctx.close()
+    # the O(sqrt K)-checkpoint mode (re-march each segment) for comparison
+    os.environ["PBE_ADJ_RECOMPUTE"] = "1"
+    ctx = pb.context_for(w)
+    times = []
+    for it in range(2):
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        ctx.run_adjoint(n0, w.c0, w.t_samples, w.target)
+        g2 = ctx.adjoint_gradient(P)
+        torch.cuda.synchronize(); times.append(time.perf_counter() - t0)
+    res.update(adjoint_recompute_ms=1e3 * min(times),
+               traj_vs_recompute_maxabs=float(np.abs(g2["grad"] - g["grad"]).max()))
+    ctx.close()
+    del os.environ["PBE_ADJ_RECOMPUTE"]
 
     # ---- forward-mode tangents: 10 lanes per pass --------------------------------------------
     passes = (P + 9) // 10

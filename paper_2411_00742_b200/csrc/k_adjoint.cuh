@@ -44,7 +44,7 @@
 namespace pbe {
 
 #if PBE_TIMING
-__device__ unsigned long long g_adj_cycles[8];    // forward, recompute, backward-vector, backward-scalar
+__device__ unsigned long long g_adj_cycles[16];    // forward, recompute, backward-vector, backward-scalar
 #define PBE_ATS(v) long long v = clock64()
 #define PBE_ATA(i, a, b) t_acc[i] += (unsigned long long)((b) - (a))
 #else
@@ -53,7 +53,10 @@ __device__ unsigned long long g_adj_cycles[8];    // forward, recompute, backwar
 #endif
 
 constexpr int ADJ_TR = 16;        // doubles per step in the scalar trace
-constexpr int ADJ_GMAX = 16;      // dL/dtheta accumulators per thread
+constexpr int ADJ_GMAX = 16;
+// physical length (doubles, even) of one padded state row of an NT-thread CTA with K bins per
+// thread: logical index x = bin + 2 in [0, NT K + 4) stored at x + x / K (host and device)
+__host__ __device__ constexpr int adj_row(int NT, int K) { return ((NT * K + 4) + (NT * K + 4) / K + 2) & ~1; }      // dL/dtheta accumulators per thread
 enum AdjTrace {
     TR_C = 0, TR_KAP2, TR_BETA2,          // Courant number, 2 kap, 2 beta (kapdot = beta Cdot)
     TR_CC, TR_CT, TR_CG,                  // dC/dc, dC/dt (total, through G), dC/dG
@@ -113,16 +116,24 @@ __device__ __forceinline__ double dG_dtheta(const KParams& kp, const double* __r
     return 0.0;
 }
 
-template <int K>
-__global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
+// NTB: the CTA width bound (256, or 512 with K = 4: 16 warps hide the per-step latency chains
+// better than 8); dL/dtheta accumulators per thread GM = ADJ_GMAX * 256 / NTB (4096 parameters)
+template <int K, int NTB = 256>
+__global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
+    constexpr int GM = ADJ_GMAX * 256 / NTB;
     const KParams& kp = ap.kp;
 #if PBE_TIMING
-    unsigned long long t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long t_acc[16] = {};
 #endif
     const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
-    const int N = kp.N, NP = NT * K + 4;
+    const int N = kp.N, NP = adj_row(NT, K);                 // physical row length (doubles)
     const int i0 = tid * K;
+    // bank-conflict-free rows: logical index x = bin + 2 lives at x + x / K, so thread t's window
+    // x = K t + j (j = 0..K+3, compile-time) sits at (K + 1) t + j + j / K -- an odd stride across
+    // the warp (K even) instead of K: 2 wavefronts per 8-byte LDS/STS instead of K (ncu: 11.7)
+    const int tb = (K + 1) * tid;
+#define PX(j) (tb + (j) + (j) / K)
     const int lim = kp.limiter;
     const double rho = kp.rho_kv;
     const int Kseg = ap.Kseg;
@@ -130,22 +141,19 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const int CP = ap.traj ? (N + 1) & ~1 : N;          // checkpoint row pitch (16-B rows for cp.async)
     double* cks = ap.ck + (size_t)s * ap.n_ck * CP;
     extern __shared__ __align__(16) double sm[];
-    double* nb = sm;                      // [2][NP] states, bin i at [i + 2]
-    double* lb = sm + 2 * NP;             // [2][NP] adjoints
+    double* nb = sm;                      // [2][NP] states, bin i at px(i + 2)
+    double* lb = sm + 2 * NP;             // [2][NP] adjoints (same layout)
     // segment states n^{k0..k1}: shared memory when they fit (host decides), else global;
-    // trajectory mode: a ring of 3 states (n^{k+1}, n^k and n^{k-1} in flight), 16-byte rows
-    const int NR = (N + 1) & ~1;
-    double* sgs = (ap.seg_smem || ap.traj) ? sm + 4 * NP : ap.seg + (size_t)s * (Kseg + 1) * N;
+    // trajectory mode: a ring of 3 states (n^{k+1}, n^k and n^{k-1} in flight); rows in the
+    // padded layout of nb (the global segment buffer too: it is this kernel's scratch)
+    double* sgs = (ap.seg_smem || ap.traj) ? sm + 4 * NP : ap.seg + (size_t)s * (Kseg + 1) * NP;
     // the segment's trace rows, staged in shared memory at every segment start
-    double* s_trs = sm + 4 * NP + (ap.traj ? (size_t)3 * NR : (ap.seg_smem ? (size_t)(Kseg + 1) * N : 0));
-    // trajectory mode: state k -> ring slot k % 3, copied by this thread's 16-byte chunks
+    double* s_trs = sm + 4 * NP + (ap.traj ? (size_t)3 * NP : (ap.seg_smem ? (size_t)(Kseg + 1) * NP : 0));
+    // trajectory mode: state k (contiguous in HBM) -> ring slot k % 3 (padded), 8-byte cp.async
     auto fetch_state = [&](long long k) {
         const double* src = cks + (size_t)k * CP;
-        double* dst = sgs + (size_t)(k % 3) * NR;
-        for (int j = 2 * tid; j < N; j += 2 * NT) {
-            if (j + 1 < N) cp_async16(dst + j, src + j);
-            else cp_async8(dst + j, src + j);
-        }
+        double* dst = sgs + (size_t)(k % 3) * NP;
+        for (int i = tid; i < N; i += NT) cp_async8(dst + (i + 2) + (i + 2) / K, src + i);
     };
     __shared__ double s_red[32][4];
     __shared__ double s_sc[12];
@@ -164,19 +172,19 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int i = i0 + k;
-            if (i < N) { const double v = n0[i]; nb[i + 2] = v; lmax = fmax(lmax, v); }
+            if (i < N) { const double v = n0[i]; nb[PX(k + 2)] = v; lmax = fmax(lmax, v); }
         }
     }
     // block sums of mu0..mu3 of nb[q] (all four if `all`, else mu3) -> s_red totals in warp 0
     auto moment_partials = [&](int q, bool all) {
         double a[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* x = nb + q * NP + 2;
+        const double* x = nb + q * NP;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int i = i0 + k;
             if (i < N) {
                 const double L = fma((double)i, kp.dL, kp.L_lo + 0.5 * kp.dL);
-                const double w0 = kp.dL * x[i], w1 = w0 * L, w2 = w1 * L;
+                const double w0 = kp.dL * x[PX(k + 2)], w1 = w0 * L, w2 = w1 * L;
                 a[3] = fma(w2, L, a[3]);
                 if (all) { a[0] += w0; a[1] += w1; a[2] += w2; }
             }
@@ -217,11 +225,11 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         return body(std::true_type{}, std::integral_constant<int, 2>{});
     };
     auto update = [&](int q, double C, double kap2, double clip) -> bool {
-        const double* in = nb + q * NP + i0;                       // in[j] = bin i0 - 2 + j
-        double* out = nb + (q ^ 1) * NP + i0 + 2;
+        const double* in = nb + q * NP;                            // in[PX(j)] = bin i0 - 2 + j
+        double* out = nb + (q ^ 1) * NP;
         double w[K + 4], F[K + 1];
 #pragma unroll
-        for (int j = 0; j < K + 4; ++j) w[j] = in[j];
+        for (int j = 0; j < K + 4; ++j) w[j] = in[PX(j)];
         with_kind(C, [&](auto negc, auto limc) {
             constexpr bool NEG = decltype(negc)::value;
 #pragma unroll
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             if (i0 + k < N) {
                 double v = (w[k + 2] - (F[k + 1] - F[k])) + 0.0;     // +0.0: canonical zero
                 if (v < 0.0) { if (v >= -clip) v = -0.0; else bad = true; }   // R-17 (mark)
-                out[k] = v;
+                out[PX(k + 2)] = v;
             }
         }
         return bad;
@@ -367,10 +375,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         if (ap.traj || k % Kseg == 0) {
             double* ckp = cks + (size_t)(ap.traj ? k : k / Kseg) * CP;
 #pragma unroll
-            for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + i0 + j + 2];
+            for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + PX(j + 2)];
         }
+        PBE_ATS(tq0);
         if (update(q, s_sc[SC_C], s_sc[SC_KAP2], clip)) s_bad = 1;
         moment_partials(q ^ 1, s_sample != 0);
+        PBE_ATS(tq1);
+        PBE_ATA(5, tq0, tq1);
         __syncthreads();
         if (poly_blk) {
             // every warp: c^{k+1} and S of the next step exactly as warp 0 forms them below
@@ -379,6 +390,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             __syncthreads();
             use_blk = true;
         }
+        PBE_ATS(tq2);
+        PBE_ATA(6, tq1, tq2);
         if (warp == 0) {
             const bool sample = s_sample != 0;
             const double mu3 = block_total(3);
@@ -412,6 +425,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             }
             if (lane == 0) { s_go = go; s_sample = go && landing; s_nsteps = nstep; s_cm[0] = c; s_cm[1] = mu3p; }
         }
+        PBE_ATS(tq3);
+        PBE_ATA(7, tq2, tq3);
         __syncthreads();
         q ^= 1;
         ++k;
@@ -419,7 +434,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     if (ap.traj) {                                         // the final state n^K closes the trajectory
         double* ckp = cks + (size_t)k * CP;
 #pragma unroll
-        for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + i0 + j + 2];
+        for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + PX(j + 2)];
     }
     PBE_ATS(tf1);
     PBE_ATA(0, tf0, tf1);
@@ -438,9 +453,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     const long long Ktot = s_nsteps;
 
     // ---- reverse pass ---------------------------------------------------------------------------
-    double gacc[ADJ_GMAX];
+    double gacc[GM];
 #pragma unroll
-    for (int g = 0; g < ADJ_GMAX; ++g) gacc[g] = 0.0;
+    for (int g = 0; g < GM; ++g) gacc[g] = 0.0;
     auto theta_accumulate = [&](double lamG, double S, double T) {
         if (kp.law == LAW_POLY) {                  // dG/da_j = (S-1)^(j+1): x^(tid+1) x (x^NT)^g
             if (!(S > 1.0)) return;
@@ -448,7 +463,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             double xp = ipow(X, tid + 1);
             const double xs = ipow(X, NT);
 #pragma unroll
-            for (int g = 0; g < ADJ_GMAX; ++g) {
+            for (int g = 0; g < GM; ++g) {
                 if (tid + g * NT < kp.n_params) gacc[g] = fma(lamG, xp, gacc[g]);
                 xp *= xs;
             }
@@ -491,21 +506,21 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
         if (!ap.traj) {
             const double* ckp = cks + (size_t)sg * N;
 #pragma unroll
-            for (int j = 0; j < K; ++j) if (i0 + j < N) nb[i0 + j + 2] = ckp[i0 + j];
+            for (int j = 0; j < K; ++j) if (i0 + j < N) nb[PX(j + 2)] = ckp[i0 + j];
             __syncthreads();
             int qq = 0;
             for (long long kk = k0; kk < k1; ++kk) {
-                double* sp = sgs + (size_t)(kk - k0) * N;
+                double* sp = sgs + (size_t)(kk - k0) * NP;
 #pragma unroll
-                for (int j = 0; j < K; ++j) if (i0 + j < N) sp[i0 + j] = nb[qq * NP + i0 + j + 2];
+                for (int j = 0; j < K; ++j) if (i0 + j < N) sp[PX(j + 2)] = nb[qq * NP + PX(j + 2)];
                 const double* r = s_trs + (size_t)(kk - k0) * ADJ_TR;
                 update(qq, r[TR_C], r[TR_KAP2], clip);
                 __syncthreads();
                 qq ^= 1;
             }
-            double* sp = sgs + (size_t)(k1 - k0) * N;
+            double* sp = sgs + (size_t)(k1 - k0) * NP;
 #pragma unroll
-            for (int j = 0; j < K; ++j) if (i0 + j < N) sp[i0 + j] = nb[qq * NP + i0 + j + 2];
+            for (int j = 0; j < K; ++j) if (i0 + j < N) sp[PX(j + 2)] = nb[qq * NP + PX(j + 2)];
         }
         if (warp == 0) pre_step(k1 - 1);
         __syncthreads();
@@ -517,20 +532,22 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
             //      lambda^kk, partial lambda_C -------------------------------------------------
             if (ap.traj && kk >= 1) { fetch_state(kk - 1); cp_async_commit(); }   // lands while we work
             if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
+            PBE_ATS(tv0);
+            PBE_ATA(8, tb0, tv0);
             const double C = s_sc[SC_C], kap2 = s_sc[SC_KAP2], beta2 = s_sc[SC_BETA2];
             const double lm = s_sc[SC_LM], l0 = s_sc[SC_L0], l1 = s_sc[SC_L1];
-            const double* nk = ap.traj ? sgs + (size_t)(kk % 3) * NR : sgs + (size_t)(kk - k0) * N;   // n^kk
-            const double* nk1 = ap.traj ? sgs + (size_t)((kk + 1) % 3) * NR : nk + N;                // n^{kk+1}
-            const double* lin = lb + ql * NP + i0;                      // lin[j] = raw lambda of bin i0-2+j
+            const double* nk = sgs + (size_t)(ap.traj ? kk % 3 : kk - k0) * NP;              // n^kk
+            const double* nk1 = ap.traj ? sgs + (size_t)((kk + 1) % 3) * NP : nk + NP;       // n^{kk+1}
+            const double* lin = lb + ql * NP;                           // lin[PX(j)] = raw lambda of bin i0-2+j
             double w[K + 4], lam[K + 4];
 #pragma unroll
             for (int j = 0; j < K + 4; ++j) {
                 const int i = i0 - 2 + j;
                 const bool in = i >= 0 && i < N;
-                w[j] = in ? nk[i] : 0.0;
-                const double v1 = in ? nk1[i] : 0.0;
+                w[j] = in ? nk[PX(j)] : 0.0;
+                const double v1 = in ? nk1[PX(j)] : 0.0;
                 const bool clipped = in && v1 == 0.0 && signbit(v1);
-                double l = lin[j];
+                double l = lin[PX(j)];
                 if (in) {
                     const double L = fma((double)i, kp.dL, kp.L_lo + 0.5 * kp.dL);
                     const double w0 = kp.dL, w1 = w0 * L, w3 = w1 * L * L;
@@ -538,6 +555,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                 }
                 lam[j] = (in && !clipped) ? l : 0.0;
             }
+            PBE_ATS(tv1);
+            PBE_ATA(9, tv0, tv1);
             // face partials (as k_resident's tangent lanes): faces f = i0 - 1 + e, e = 0..K+2
             double Lf[K + 3], whi[K + 3], wmid[K + 3], wlo[K + 3];
             double lamC = 0.0;
@@ -564,7 +583,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                     if (owned) lamC = fma(Lf[e], fma(beta2, h, nup), lamC); // dF/dC = n_up + beta psi
                 }
             });
-            double* lout = lb + (ql ^ 1) * NP + i0 + 2;
+            PBE_ATS(tv2);
+            PBE_ATA(10, tv1, tv2);
+            double* lout = lb + (ql ^ 1) * NP;
 #pragma unroll
             for (int kq = 0; kq < K; ++kq) {
                 if (i0 + kq >= N) continue;
@@ -572,11 +593,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
                 double v = lam[kq + 2];
                 if (C >= 0.0) v += Lf[e] * whi[e] + Lf[e + 1] * wmid[e + 1] + Lf[e + 2] * wlo[e + 2];
                 else          v += Lf[e + 1] * wlo[e + 1] + Lf[e] * wmid[e] + Lf[e - 1] * whi[e - 1];
-                lout[kq] = v;
+                lout[PX(kq + 2)] = v;
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) lamC += __shfl_xor_sync(0xffffffffu, lamC, off);
             if (lane == 0) s_red[warp][0] = lamC;
+            PBE_ATS(tv3);
+            PBE_ATA(11, tv2, tv3);
             __syncthreads();
             PBE_ATS(tb1);
             PBE_ATA(2, tb0, tb1);
@@ -605,13 +628,14 @@ __global__ void __launch_bounds__(256) k_adjoint(const AdjParams ap) {
     }
     if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
 #pragma unroll
-    for (int g = 0; g < ADJ_GMAX; ++g) {
+    for (int g = 0; g < GM; ++g) {
         const int j = tid + g * NT;
         if (j < kp.n_params) ap.gtheta[(size_t)s * kp.n_params + j] = gacc[g];
     }
 #if PBE_TIMING
-    if (blockIdx.x == 0 && tid == 0) { t_acc[4] = (unsigned long long)Ktot; for (int i = 0; i < 8; ++i) g_adj_cycles[i] = t_acc[i]; }
+    if (blockIdx.x == 0 && tid == 0) { t_acc[4] = (unsigned long long)Ktot; for (int i = 0; i < 16; ++i) g_adj_cycles[i] = t_acc[i]; }
 #endif
 }
 
+#undef PX
 }  // namespace pbe

@@ -623,10 +623,11 @@ static KParams make_kparams(pbe_ctx ctx, int n_sims, const double* n0_dev, long 
 // ------------------------------------------------------------------------------------
 // k_adjoint launch (NEXT-3): one CTA per simulation; K from N (smem: 4 (NT K + 4) doubles)
 // ------------------------------------------------------------------------------------
-struct AdjointVariant { int K; const void* fn; };
+struct AdjointVariant { int K, ntb; const void* fn; };
 const AdjointVariant kAdjoint[] = {
-    {4, (const void*)&pbe::k_adjoint<4>}, {8, (const void*)&pbe::k_adjoint<8>},
-    {16, (const void*)&pbe::k_adjoint<16>}, {24, (const void*)&pbe::k_adjoint<24>},
+    {4, 256, (const void*)&pbe::k_adjoint<4>}, {8, 256, (const void*)&pbe::k_adjoint<8>},
+    {4, 512, (const void*)&pbe::k_adjoint<4, 512>},   // PBE_ADJ_K=4 A/B only (N = 2000: 99 vs 87 ms)
+    {16, 256, (const void*)&pbe::k_adjoint<16>}, {24, 256, (const void*)&pbe::k_adjoint<24>},
 };
 
 // ------------------------------------------------------------------------------------
@@ -1008,31 +1009,34 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     const AdjointVariant* av = nullptr;
     int nt = 0;
     size_t smem = 0;
+    const int force_k = getenv("PBE_ADJ_K") ? atoi(getenv("PBE_ADJ_K")) : 0;   // A/B only
     for (const auto& v : kAdjoint) {
         const int t = ((N + v.K - 1) / v.K + 31) / 32 * 32;
-        const size_t sm = (size_t)4 * (t * v.K + 4) * sizeof(double);
-        if (t <= 256 && sm <= 200 * 1024) { av = &v; nt = t; smem = sm; break; }
+        const size_t sm = (size_t)4 * pbe::adj_row(t, v.K) * sizeof(double);
+        if (force_k && v.K != force_k) continue;
+        if (t <= v.ntb && sm <= 212 * 1024 && ctx->n_params <= t * (pbe::ADJ_GMAX * 256 / v.ntb)) {
+            av = &v; nt = t; smem = sm; break;
+        }
     }
-    if (!av) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: N = %d exceeds the adjoint kernel (N <= 6144)", N);
-    if (ctx->n_params > nt * pbe::ADJ_GMAX)
-        return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: %d parameters exceed %d for N = %d", ctx->n_params, nt * pbe::ADJ_GMAX, N);
+    if (!av) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: N = %d with %d parameters exceeds the adjoint kernel "
+                                           "(N <= 6144, n_params <= 16 x the CTA size)", N, ctx->n_params);
     const long long ms = cf.max_steps;
     // segment length: the segment's trace rows are staged in shared memory every segment, and
     // its states n^{k0..k1} live there too when they fit (else in a global buffer)
-    const size_t smem_cap = 220 * 1024, row = (size_t)N * sizeof(double), trow = pbe::ADJ_TR * sizeof(double);
+    const size_t smem_cap = 220 * 1024, row = (size_t)pbe::adj_row(nt, av->K) * sizeof(double), trow = pbe::ADJ_TR * sizeof(double);
     int Kseg = checkpoint_every;
     // checkpoint_every = 0 (auto): keep the whole trajectory in HBM when it takes <= 16 GB (C5-size
     // NEXT-3: 9 x 12,001 x 2000 doubles = 1.7 GB) -- no re-march in the reverse pass; else O(sqrt)
     const int NRr = (N + 1) & ~1;
     const bool traj = checkpoint_every == 0 &&
                       (double)n_sims * (ms + 1) * N * sizeof(double) <= 16.0 * (1ull << 30) &&
-                      smem + (size_t)3 * NRr * sizeof(double) + 64 * (size_t)pbe::ADJ_TR * sizeof(double) <= 220 * 1024 &&
+                      smem + 3 * row + 64 * (size_t)pbe::ADJ_TR * sizeof(double) <= 220 * 1024 &&
                       !getenv("PBE_ADJ_RECOMPUTE");
     if (Kseg == 0) Kseg = std::max(8, (int)std::ceil(std::sqrt((double)ms)));       // O(sqrt) memory
     int seg_smem = 0;
     if (traj) {
         Kseg = 64;                                        // trace rows staged per segment
-        smem += (size_t)3 * NRr * sizeof(double);
+        smem += 3 * row;
     } else {
         // largest K' <= Kseg with the states in shared memory; take it when K' >= min(Kseg, 4)
         long long kfit = ((long long)smem_cap - (long long)smem - (long long)row) / (long long)(row + trow);
@@ -1047,7 +1051,7 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     const long long n_ck = traj ? ms + 1 : (ms + Kseg - 1) / Kseg;
     const size_t tr_b = (size_t)n_sims * ms * pbe::ADJ_TR * sizeof(double);
     const size_t ck_b = (size_t)n_sims * n_ck * (traj ? NRr : N) * sizeof(double);
-    const size_t sg_b = (seg_smem || traj) ? sizeof(double) : (size_t)n_sims * (Kseg + 1) * N * sizeof(double);
+    const size_t sg_b = (seg_smem || traj) ? sizeof(double) : (size_t)n_sims * (Kseg + 1) * row;
     if ((double)tr_b + ck_b + sg_b > 64.0 * (1ull << 30))
         return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: trace + checkpoints need %.1f GB (> 64 GB): lower max_steps or n_sims",
                     ((double)tr_b + ck_b + sg_b) / (1ull << 30));

@@ -143,6 +143,14 @@ def test_adjoint_trajectory_mode_matches_recompute_mode(N, monkeypatch):
     assert np.array_equal(g0["grad"], g1["grad"]) and np.array_equal(g0["loss"], g1["loss"])
 
 
+@pytest.mark.parametrize("N", [1500, 3001, 6000])
+def test_adjoint_large_mesh_matches_oracle(N):
+    """The wider CTA variants (K = 4 at 384-512 threads, K = 16, K = 24 at 256 threads) with
+    their padded shared-memory rows; N = 6000 also takes the segment re-march (the 3-state ring
+    does not fit next to the K = 24 rows)."""
+    _check(small_ensemble(n_sims=2, N=N, t_max=4.0, M=4))
+
+
 def test_adjoint_agrees_with_gpu_tangents():
     """The two GPU differentiation modes (k_resident tangent lanes, k_adjoint) agree."""
     import paper_2411_00742_b200 as pb

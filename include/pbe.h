@@ -183,8 +183,9 @@ pbe_status pbe_tangents(pbe_ctx ctx, double* tangents, double* grad, int32_t on_
  *                     states) are staged in shared memory; device memory per simulation =
  *                     8 B x (16 max_steps + N ceil(max_steps / K) [+ N (K + 1) if the states
  *                     do not fit shared memory]) -- max_steps bounds the trace
- * Restrictions (PBE_ERR_ARG): 1D model, sample mode (n_steps = 0), N <= 6144, n_params <=
- * 16 x the CTA size.  The gradient is w.r.t. theta only (not the solubility parameters).
+ * Restrictions (PBE_ERR_ARG): 1D model, sample mode (n_steps = 0), N <= 6144.  The gradient is
+ * w.r.t. theta only (not the solubility parameters).  Launches k_adjoint (one CTA per simulation)
+ * and k_adjoint_theta (dL/dtheta from the per-step trace, grid over parameters x simulations).
  * Records, status, steps and loss of the forward pass are read with pbe_moments. */
 pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_t n0_stride,
                            int32_t n0_on_device, const double* c0, const double* t_samples,

@@ -53,16 +53,16 @@ __device__ unsigned long long g_adj_cycles[16];    // forward, recompute, backwa
 #endif
 
 constexpr int ADJ_TR = 16;        // doubles per step in the scalar trace
-constexpr int ADJ_GMAX = 16;
 // physical length (doubles, even) of one padded state row of an NT-thread CTA with K bins per
 // thread: logical index x = bin + 2 in [0, NT K + 4) stored at x + x / K (host and device)
-__host__ __device__ constexpr int adj_row(int NT, int K) { return ((NT * K + 4) + (NT * K + 4) / K + 2) & ~1; }      // dL/dtheta accumulators per thread
+__host__ __device__ constexpr int adj_row(int NT, int K) { return ((NT * K + 4) + (NT * K + 4) / K + 2) & ~1; }
 enum AdjTrace {
     TR_C = 0, TR_KAP2, TR_BETA2,          // Courant number, 2 kap, 2 beta (kapdot = beta Cdot)
     TR_CC, TR_CT, TR_CG,                  // dC/dc, dC/dt (total, through G), dC/dG
     TR_TC, TR_TT, TR_TG,                  // dt'/dc, dt'/dt, dt'/dG   (t' = t^{k+1})
     TR_S, TR_T,                           // supersaturation and temperature of the step
-    TR_LC, TR_L0, TR_L1                   // d loss / d(c, mu0, mu1)(n^{k+1}) if step k lands on a sample
+    TR_LC, TR_L0, TR_L1,                  // d loss / d(c, mu0, mu1)(n^{k+1}) if step k lands on a sample
+    TR_LG                                 // lambda_G^k, the adjoint of G^k (written by the reverse pass)
 };
 
 struct AdjParams {
@@ -116,11 +116,9 @@ __device__ __forceinline__ double dG_dtheta(const KParams& kp, const double* __r
     return 0.0;
 }
 
-// NTB: the CTA width bound (256, or 512 with K = 4: 16 warps hide the per-step latency chains
-// better than 8); dL/dtheta accumulators per thread GM = ADJ_GMAX * 256 / NTB (4096 parameters)
+// NTB: the CTA width bound (256; 512 with K = 4 is an A/B variant)
 template <int K, int NTB = 256>
 __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
-    constexpr int GM = ADJ_GMAX * 256 / NTB;
     const KParams& kp = ap.kp;
 #if PBE_TIMING
     unsigned long long t_acc[16] = {};
@@ -445,7 +443,6 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         s_ok = status == ST_OK;
     }
     __syncthreads();
-    const double* th = kp.theta + (size_t)s * kp.n_params;
     if (!s_ok) {
         for (int j = tid; j < kp.n_params; j += NT) ap.gtheta[(size_t)s * kp.n_params + j] = __longlong_as_double(0x7ff8000000000000ll);
         return;
@@ -453,24 +450,8 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     const long long Ktot = s_nsteps;
 
     // ---- reverse pass ---------------------------------------------------------------------------
-    double gacc[GM];
-#pragma unroll
-    for (int g = 0; g < GM; ++g) gacc[g] = 0.0;
-    auto theta_accumulate = [&](double lamG, double S, double T) {
-        if (kp.law == LAW_POLY) {                  // dG/da_j = (S-1)^(j+1): x^(tid+1) x (x^NT)^g
-            if (!(S > 1.0)) return;
-            const double X = S - 1.0;
-            double xp = ipow(X, tid + 1);
-            const double xs = ipow(X, NT);
-#pragma unroll
-            for (int g = 0; g < GM; ++g) {
-                if (tid + g * NT < kp.n_params) gacc[g] = fma(lamG, xp, gacc[g]);
-                xp *= xs;
-            }
-            return;
-        }
-        for (int j = tid; j < kp.n_params && j < 6; j += NT) gacc[0] = fma(lamG, dG_dtheta(kp, th, S, T, j), gacc[0]);
-    };
+    // dL/dtheta_j = sum_k lambda_G^k dG^k/dtheta_j is left to k_adjoint_theta (the whole GPU, after
+    // this kernel): the reverse pass only records lambda_G^k in the trace
     // warp-0 adjoint scalars: of c^{k+1} (before the sample term of step k), t^{k+1}, mu3p^{k+1}
     double lam_c = 0.0, lam_t = 0.0, lam_mu = 0.0;
     long long k0s = 0;                             // first step of the staged trace segment
@@ -484,8 +465,6 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         }
     };
     int ql = 0;                                    // lb[ql] = lambda of n^{k+1} (raw)
-    bool have_lg = false;
-    double lg_prev = 0.0, S_prev = 0.0, T_prev = 0.0;
     const long long nseg = (Ktot + Kseg - 1) / Kseg;
     if (ap.traj && Ktot > 0) {                             // n^K and n^{K-1} before the first step
         __syncthreads();                                   // the final state's global stores are done
@@ -531,7 +510,6 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
             // ---- vector phase: lambda^{kk+1} (+ mass-balance and sample terms, clip marks) ->
             //      lambda^kk, partial lambda_C -------------------------------------------------
             if (ap.traj && kk >= 1) { fetch_state(kk - 1); cp_async_commit(); }   // lands while we work
-            if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
             PBE_ATS(tv0);
             PBE_ATA(8, tb0, tv0);
             const double C = s_sc[SC_C], kap2 = s_sc[SC_KAP2], beta2 = s_sc[SC_BETA2];
@@ -613,24 +591,16 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                 const double lG = LC * r[TR_CG] + lam_t * r[TR_TG];
                 lam_mu = rho * lcp;
                 lam_c = nc; lam_t = nt;
-                if (lane == 0) { s_sc[SC_LG] = lG; s_sc[SC_S] = r[TR_S]; s_sc[SC_T] = r[TR_T]; }
+                if (lane == 0) trs[(size_t)kk * ADJ_TR + TR_LG] = lG;
                 if (kk > k0) pre_step(kk - 1);
             }
             if (ap.traj) asm volatile("cp.async.wait_group 0;" ::: "memory");   // n^{kk-1}: this thread's part
             __syncthreads();
-            lg_prev = s_sc[SC_LG]; S_prev = s_sc[SC_S]; T_prev = s_sc[SC_T];
-            have_lg = true;
             ql ^= 1;
             PBE_ATS(tb2);
             PBE_ATA(3, tb1, tb2);
         }
         __syncthreads();
-    }
-    if (have_lg) theta_accumulate(lg_prev, S_prev, T_prev);
-#pragma unroll
-    for (int g = 0; g < GM; ++g) {
-        const int j = tid + g * NT;
-        if (j < kp.n_params) ap.gtheta[(size_t)s * kp.n_params + j] = gacc[g];
     }
 #if PBE_TIMING
     if (blockIdx.x == 0 && tid == 0) { t_acc[4] = (unsigned long long)Ktot; for (int i = 0; i < 16; ++i) g_adj_cycles[i] = t_acc[i]; }
@@ -638,4 +608,43 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
 }
 
 #undef PX
+
+// dL/dtheta_j = sum_{k < K} lambda_G^k dG/dtheta_j(S^k, T^k) from the trace rows (TR_LG, TR_S,
+// TR_T) of every simulation whose march succeeded (failed ones keep the NaN k_adjoint wrote).
+// Grid (ceil(n_params / 32), n_sims), 256 threads: lane = parameter j within the block's 32, the
+// 8 warps take contiguous step chunks, partials summed in warp order (deterministic).  POLY:
+// dG/da_j = (S - 1)^(j+1) for S > 1 (ipow); other laws: dG_dtheta.
+__global__ void __launch_bounds__(256) k_adjoint_theta(const AdjParams ap) {
+    const KParams& kp = ap.kp;
+    const int s = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + lane;
+    if (kp.status[s] != ST_OK) return;
+    const long long Ktot = kp.steps[s];
+    const double* trs = ap.tr + (size_t)s * kp.max_steps * ADJ_TR;
+    const double* th = kp.theta + (size_t)s * kp.n_params;
+    const long long ch = (Ktot + 7) / 8, ka = warp * ch, kb = min(Ktot, ka + ch);
+    double acc = 0.0;
+    if (j < kp.n_params) {
+        if (kp.law == LAW_POLY) {
+            for (long long k = kb - 1; k >= ka; --k) {
+                const double* r = trs + (size_t)k * ADJ_TR;
+                const double S = __ldg(r + TR_S);
+                if (S > 1.0) acc = fma(__ldg(r + TR_LG), ipow(S - 1.0, j + 1), acc);
+            }
+        } else if (j < 6) {
+            for (long long k = kb - 1; k >= ka; --k) {
+                const double* r = trs + (size_t)k * ADJ_TR;
+                acc = fma(__ldg(r + TR_LG), dG_dtheta(kp, th, __ldg(r + TR_S), __ldg(r + TR_T), j), acc);
+            }
+        }
+    }
+    __shared__ double red[8][32];
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && j < kp.n_params) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w][lane];
+        ap.gtheta[(size_t)s * kp.n_params + j] = t;
+    }
+}
 }  // namespace pbe

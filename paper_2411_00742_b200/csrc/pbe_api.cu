@@ -1014,12 +1014,11 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
         const int t = ((N + v.K - 1) / v.K + 31) / 32 * 32;
         const size_t sm = (size_t)4 * pbe::adj_row(t, v.K) * sizeof(double);
         if (force_k && v.K != force_k) continue;
-        if (t <= v.ntb && sm <= 212 * 1024 && ctx->n_params <= t * (pbe::ADJ_GMAX * 256 / v.ntb)) {
+        if (t <= v.ntb && sm <= 212 * 1024) {
             av = &v; nt = t; smem = sm; break;
         }
     }
-    if (!av) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: N = %d with %d parameters exceeds the adjoint kernel "
-                                           "(N <= 6144, n_params <= 16 x the CTA size)", N, ctx->n_params);
+    if (!av) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: N = %d exceeds the adjoint kernel (N <= 6144)", N);
     const long long ms = cf.max_steps;
     // segment length: the segment's trace rows are staged in shared memory every segment, and
     // its states n^{k0..k1} live there too when they fit (else in a global buffer)
@@ -1077,9 +1076,13 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     CUDA_TRY(ctx, cudaLaunchKernel(av->fn, dim3(n_sims), dim3(nt), args, smem, st));
     CUDA_TRY(ctx, cudaGetLastError());
+    if (ctx->n_params > 0) {
+        pbe::k_adjoint_theta<<<dim3((ctx->n_params + 31) / 32, n_sims), 256, 0, st>>>(ap);
+        CUDA_TRY(ctx, cudaGetLastError());
+    }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
     ctx->info.kernel = PBE_KERNEL_ADJOINT;
-    ctx->info.launches = 1;
+    ctx->info.launches = ctx->n_params > 0 ? 2 : 1;
     ctx->info.threads_per_cta = nt;
     ctx->info.ctas = n_sims;
     ctx->info.cluster = 1;

@@ -37,6 +37,7 @@
 //  double-buffered by step parity; warp 0 runs the scalar phases (two barriers per step).
 // =====================================================================================
 #pragma once
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "pbe_device.cuh"
@@ -92,6 +93,38 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
+// cluster mode: remote shared-memory stores that complete bytes on the RECEIVER's mbarrier
+// (st.async), so each CTA waits only for the data it needs instead of a cluster-wide barrier
+__device__ __forceinline__ unsigned adj_mapa(const void* p, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void adj_st_async2(unsigned raddr, double a, double b, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr), "d"(a), "d"(b), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void adj_st_async1(unsigned raddr, double a, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+                 ::"r"(raddr), "d"(a), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void adj_mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void adj_mbar_arrive(unsigned long long* bar, unsigned tx) {
+    if (tx)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(tx) : "memory");
+    else
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void adj_mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+
 // dG/dtheta_j at (S, T) in closed form (the parameters enter the laws of growth_rate as
 // below; dpow(x, y) = exp(y log x) there).
 __device__ __forceinline__ double dG_dtheta(const KParams& kp, const double* __restrict__ th, double S, double T, int j) {
@@ -116,17 +149,30 @@ __device__ __forceinline__ double dG_dtheta(const KParams& kp, const double* __r
     return 0.0;
 }
 
-// NTB: the CTA width bound (256; 512 with K = 4 is an A/B variant)
-template <int K, int NTB = 256>
+// NTB: the CTA width bound (256; 512 with K = 4 is an A/B variant).
+// CL: a thread-block cluster of CS CTAs per simulation (trajectory mode only), CTA r holding bins
+// [r NT K, (r + 1) NT K): edge bins and edge adjoints are pushed into the neighbours' ghost cells
+// over DSMEM, warp/CTA partial sums are added across the cluster in a fixed order by every CTA
+// (so every CTA runs the identical scalar chain and no broadcast is needed), the step barrier
+// after the partials is cluster.sync(), and rank 0 alone writes the trace and the records.
+// NEXT-3 at N = 2000 on 9 experiments: 16 CTAs each = 144 SMs instead of 9.
+template <int K, int NTB = 256, bool CL = false>
 __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
+    namespace cg = cooperative_groups;
     const KParams& kp = ap.kp;
 #if PBE_TIMING
     unsigned long long t_acc[16] = {};
 #endif
-    const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int CS = CL ? (int)cg::this_cluster().num_blocks() : 1;
+    const int rank = CL ? (int)cg::this_cluster().block_rank() : 0;
+    const int s = blockIdx.x / CS, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5;
     const int N = kp.N, NP = adj_row(NT, K);                 // physical row length (doubles)
-    const int i0 = tid * K;
+    const int NB = NT * K, b0 = rank * NB;                   // this CTA's bins [b0, b0 + NB)
+    const int i0 = b0 + tid * K;                             // global index of the thread's first bin
+    auto cl_sync = [&]() __attribute__((always_inline)) {
+        if constexpr (CL) cg::this_cluster().sync(); else __syncthreads();
+    };
     // bank-conflict-free rows: logical index x = bin + 2 lives at x + x / K, so thread t's window
     // x = K t + j (j = 0..K+3, compile-time) sits at (K + 1) t + j + j / K -- an odd stride across
     // the warp (K even) instead of K: 2 wavefronts per 8-byte LDS/STS instead of K (ncu: 11.7)
@@ -148,22 +194,36 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     // the segment's trace rows, staged in shared memory at every segment start
     double* s_trs = sm + 4 * NP + (ap.traj ? (size_t)3 * NP : (ap.seg_smem ? (size_t)(Kseg + 1) * NP : 0));
     // trajectory mode: state k (contiguous in HBM) -> ring slot k % 3 (padded), 8-byte cp.async
+    // (local index x = bin - b0 + 2, ghost/halo bins included)
     auto fetch_state = [&](long long k) {
         const double* src = cks + (size_t)k * CP;
         double* dst = sgs + (size_t)(k % 3) * NP;
-        for (int i = tid; i < N; i += NT) cp_async8(dst + (i + 2) + (i + 2) / K, src + i);
+        for (int x = tid; x < NB + 4; x += NT) {
+            const int i = b0 - 2 + x;
+            if (i >= 0 && i < N) cp_async8(dst + x + x / K, src + i);
+        }
     };
-    __shared__ double s_red[32][4];
+    // warp partials, double-buffered by step parity: [par][rank NW + warp][m] -- in CL mode every
+    // warp pushes its partials into EVERY CTA of the cluster (remote stores do not stall), so the
+    // reads after the cluster barrier are local
+    // slots: mu0..mu3 (or lambda_C, 0, 0, 0), the warp's clip-failure flag, pad
+    __shared__ __align__(16) double s_red[2][32][6];
+    __shared__ unsigned long long s_mbar[2];       // CL: one mbarrier per parity (partials + halos)
+    unsigned mph = 0;                              // CL: phase bit of s_mbar[0], s_mbar[1]
     __shared__ double s_sc[12];
     __shared__ double s_pp[32][2];                 // long polynomial: per-warp (G, dG/dx) partials
     __shared__ double s_cm[2];                     // warp 0's c, mu3p (read by every warp)
-    __shared__ int s_go, s_sample, s_bad, s_ok;
+    __shared__ int s_go, s_sample, s_ok;
     __shared__ long long s_nsteps;
     enum { SC_C = 0, SC_KAP2, SC_BETA2, SC_LM, SC_L0, SC_L1, SC_LG, SC_S, SC_T, SC_CLIP };
 
     for (int j = tid; j < 4 * NP; j += NT) sm[j] = 0.0;
-    if (tid == 0) s_bad = 0;
-    __syncthreads();
+    if (CL && tid == 0) {
+        adj_mbar_init(&s_mbar[0], NW);             // every local warp arrives once per phase
+        adj_mbar_init(&s_mbar[1], NW);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl_sync();                                     // CL: the barriers exist before any remote store
     double lmax = 0.0;
     {
         const double* n0 = kp.n0 + (size_t)s * kp.n0_stride;
@@ -172,10 +232,73 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
             const int i = i0 + k;
             if (i < N) { const double v = n0[i]; nb[PX(k + 2)] = v; lmax = fmax(lmax, v); }
         }
+        if (CL && tid < 4) {                       // halo bins b0-2, b0-1, b0+NB, b0+NB+1
+            const int x = tid < 2 ? tid : NB + tid;
+            const int i = b0 - 2 + x;
+            if (i >= 0 && i < N) nb[x + x / K] = n0[i];
+        }
     }
-    // block sums of mu0..mu3 of nb[q] (all four if `all`, else mu3) -> s_red totals in warp 0
-    auto moment_partials = [&](int q, bool all) {
-        double a[4] = {0.0, 0.0, 0.0, 0.0};
+    // cluster neighbours' shared memory (DSMEM): the same offset in CTA rank r
+    auto remote = [&](auto* p, int r) -> decltype(p) {
+        if constexpr (CL) return cg::this_cluster().map_shared_rank(p, r);
+        else return p;
+    };
+    // push this CTA's two edge values of row `row` into the neighbours' ghost cells (CL only),
+    // completing 16 bytes on the neighbour's mbarrier of parity par (two 8-byte st.async: the
+    // padded ghost pair is not always 16-byte aligned)
+    auto push_halo = [&](double* row, int par) __attribute__((always_inline)) {
+        if constexpr (CL) {
+            if (tid == 0 && rank > 0) {            // local bins 0, 1 -> left neighbour's x = NB+2, NB+3
+                const unsigned rb = adj_mapa(&s_mbar[par], rank - 1);
+                adj_st_async1(adj_mapa(row + (NB + 2) + (NB + 2) / K, rank - 1), row[2 + 2 / K], rb);
+                adj_st_async1(adj_mapa(row + (NB + 3) + (NB + 3) / K, rank - 1), row[3 + 3 / K], rb);
+            }
+            if (tid == NT - 1 && rank < CS - 1) {  // local bins NB-2, NB-1 -> right neighbour's x = 0, 1
+                const unsigned rb = adj_mapa(&s_mbar[par], rank + 1);
+                adj_st_async1(adj_mapa(row, rank + 1), row[NB + NB / K], rb);
+                adj_st_async1(adj_mapa(row + 1, rank + 1), row[(NB + 1) + (NB + 1) / K], rb);
+            }
+        }
+    };
+    // this warp's partials a[0..4] (identical in every lane after a butterfly) -> slot
+    // rank NW + warp of every CTA (lane r stores to rank r; remote ones with st.async)
+    auto put_partials = [&](int par, const double* a) __attribute__((always_inline)) {
+        if constexpr (CL) {
+            double* d = &s_red[par][rank * NW + warp][0];
+            if (lane == rank) {
+#pragma unroll
+                for (int m = 0; m < 5; ++m) d[m] = a[m];
+            } else if (lane < CS) {
+                const unsigned rb = adj_mapa(&s_mbar[par], lane);
+                adj_st_async2(adj_mapa(d, lane), a[0], a[1], rb);
+                adj_st_async2(adj_mapa(d + 2, lane), a[2], a[3], rb);
+                adj_st_async2(adj_mapa(d + 4, lane), a[4], 0.0, rb);
+            }
+        } else if (lane == 0) {
+#pragma unroll
+            for (int m = 0; m < 5; ++m) s_red[par][warp][m] = a[m];
+        }
+    };
+    // the exchange point of a step: the partials of parity par (and, with halo, the neighbours'
+    // edge values) of every CTA are in place.  CL: each warp arrives on the local mbarrier (warp 0
+    // also posts the expected remote bytes) and every thread waits for the phase; else a CTA barrier.
+    auto exchange = [&](int par, bool halo) __attribute__((always_inline)) {
+        if constexpr (CL) {
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned tx = (unsigned)((CS - 1) * NW * 48) +
+                                    (halo ? 16u * ((rank > 0) + (rank < CS - 1)) : 0u);
+                adj_mbar_arrive(&s_mbar[par], warp == 0 ? tx : 0u);
+            }
+            adj_mbar_wait(&s_mbar[par], (mph >> par) & 1u);
+            mph ^= 1u << par;
+        } else {
+            __syncthreads();
+        }
+    };
+    // block sums of mu0..mu3 of nb[q] (all four if `all`, else mu3) -> s_red[par] (warp partials)
+    auto moment_partials = [&](int q, bool all, int par, const double* slot0 = nullptr, bool bad = false) {
+        double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         const double* x = nb + q * NP;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -191,15 +314,32 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
             for (int m = 0; m < 4; ++m) a[m] += __shfl_xor_sync(0xffffffffu, a[m], off);
-        if (lane == 0)
-#pragma unroll
-            for (int m = 0; m < 4; ++m) s_red[warp][m] = a[m];
+        if (slot0) a[0] = *slot0;
+        a[4] = __any_sync(0xffffffffu, bad) ? 1.0 : 0.0;
+        put_partials(par, a);
     };
-    auto block_total = [&](int m) -> double {                      // warp 0, after a barrier
+    // total (or max) of slot m of the partials s_red[par] over the CTA -- over the cluster in CL
+    // mode (lane e loads partial e % NW of rank e / NW, then a butterfly: identical in every lane
+    // and every CTA).  Whole warps, after the barrier that follows the partials.
+    auto red_total = [&](int m, int par, bool mx) -> double {
         double t = 0.0;
-        for (int w = 0; w < NW; ++w) t += s_red[w][m];
+        if constexpr (!CL) {
+            for (int w = 0; w < NW; ++w) t = mx ? fmax(t, s_red[par][w][m]) : t + s_red[par][w][m];
+        } else {
+            for (int e = lane; e < CS * NW; e += 32) {
+                const double v = s_red[par][e][m];
+                t = mx ? fmax(t, v) : t + v;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double o = __shfl_xor_sync(0xffffffffu, t, off);
+                t = mx ? fmax(t, o) : t + o;
+            }
+        }
         return t;
     };
+    int rpar = 0;                                   // parity of the partials being read
+    auto block_total = [&](int m) -> double { return red_total(m, rpar, false); };
     // forward update nb[q] -> nb[q^1] (eq-highRes_growth, flux form; clip marks as -0.0)
     // limited half slope of kind LIMT (0 upwind, 1 van Leer branch-free, 2 minmod/superbee/MC):
     // the sweep direction and the limiter are resolved once per step, not per face (a branch per
@@ -254,11 +394,10 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         return bad;
     };
 
-    moment_partials(0, false);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-    if (lane == 0) s_red[warp][0] = lmax;          // mu0 slot reused for max(n0) (mu3 in slot 3)
-    __syncthreads();
+    moment_partials(0, false, 0, &lmax);           // mu0 slot reused for max(n0) (mu3 in slot 3)
+    exchange(0, false);
 
     // ---- warp-0 scalar state of the forward pass ----------------------------------------------
     const KinLoader KL{kp.theta + (size_t)s * kp.n_params, kp.sol, kp.seed, -1, kp.n_params, kp.n_params + kp.n_sol};
@@ -278,9 +417,32 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     // warp-cooperative form.
     const bool poly_blk = kp.law == LAW_POLY && kp.n_params > MAXTH && KC.const_T;
     bool use_blk = false;                                  // warp 0: the partials of this step are ready
+    // coefficients a_j of this thread's terms [tid PM, tid PM + PM) kept in registers for the
+    // march when n_params <= NT PM (an L1 miss per term per step otherwise: 4.6k cycles/step
+    // at 64 threads x 16 terms)
+    constexpr int PM = (1024 + NTB - 1) / NTB;
+    const bool poly_reg = poly_blk && kp.n_params <= NT * PM;
+    double pc[PM];
+#pragma unroll
+    for (int i = 0; i < PM; ++i) {
+        const int j = tid * PM + i;
+        pc[i] = poly_reg && j < kp.n_params ? kp.theta[(size_t)s * kp.n_params + j] : 0.0;
+    }
     auto poly_partials = [&](double Sv) {                  // every thread, after the step's barrier
         double tt = 0.0, dtt = 0.0;
-        if (Sv > 1.0) {
+        if (Sv > 1.0 && poly_reg) {
+            const double x = Sv - 1.0;
+            const int j0 = tid * PM;
+            double qv = 0.0, dq = 0.0;
+#pragma unroll
+            for (int i = PM - 1; i >= 0; --i) {
+                dq = fma(dq, x, qv);
+                qv = fma(qv, x, pc[i]);
+            }
+            const double xl = ipow(x, j0);
+            tt = xl * x * qv;
+            dtt = xl * fma((double)(j0 + 1), qv, x * dq);
+        } else if (Sv > 1.0) {
             const double x = Sv - 1.0;
             const int mm = (kp.n_params + NT - 1) / NT, j0 = tid * mm;
             const double* a = kp.theta + (size_t)s * kp.n_params;
@@ -327,23 +489,22 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         const double dC2 = __shfl_sync(0xffffffffu, sc.C.d, 2);
         const double dT0 = __shfl_sync(0xffffffffu, tp.d, 0), dT1 = __shfl_sync(0xffffffffu, tp.d, 1);
         const double dT2 = __shfl_sync(0xffffffffu, tp.d, 2);
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             double* r = trs + (size_t)k * ADJ_TR;
             r[TR_C] = Cv; r[TR_KAP2] = 2.0 * sc.kap.v; r[TR_BETA2] = 2.0 * beta;
             r[TR_CC] = dC0; r[TR_CT] = dC1; r[TR_CG] = dC2;
             r[TR_TC] = dT0; r[TR_TT] = dT1; r[TR_TG] = dT2;
             r[TR_S] = S.v; r[TR_T] = T.v;
             r[TR_LC] = 0.0; r[TR_L0] = 0.0; r[TR_L1] = 0.0;
-            s_sc[SC_C] = Cv; s_sc[SC_KAP2] = 2.0 * sc.kap.v;
         }
+        if (lane == 0) { s_sc[SC_C] = Cv; s_sc[SC_KAP2] = 2.0 * sc.kap.v; }
         dt = sc.dt.v;
         landing = sc.landing;
         return true;
     };
     if (warp == 0) {
-        double nmax = 0.0;
-        for (int w = 0; w < NW; ++w) nmax = fmax(nmax, s_red[w][0]);
-        mu3p = block_total(3);
+        const double nmax = red_total(0, 0, true);
+        mu3p = red_total(3, 0, false);
         double sc2 = 0.0, sl2 = 0.0;
         for (int j = lane; j < kp.M; j += 32) { sc2 += tgt[2 * j] * tgt[2 * j]; sl2 += tgt[2 * j + 1] * tgt[2 * j + 1]; }
 #pragma unroll
@@ -376,11 +537,14 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
             for (int j = 0; j < K; ++j) if (i0 + j < N) ckp[i0 + j] = nb[q * NP + PX(j + 2)];
         }
         PBE_ATS(tq0);
-        if (update(q, s_sc[SC_C], s_sc[SC_KAP2], clip)) s_bad = 1;
-        moment_partials(q ^ 1, s_sample != 0);
+        const bool bad = update(q, s_sc[SC_C], s_sc[SC_KAP2], clip);
+        const int par = (int)((k + 1) & 1);
+        push_halo(nb + (q ^ 1) * NP, par);
+        moment_partials(q ^ 1, s_sample != 0, par, nullptr, bad);
         PBE_ATS(tq1);
         PBE_ATA(5, tq0, tq1);
-        __syncthreads();
+        exchange(par, true);
+        rpar = par;
         if (poly_blk) {
             // every warp: c^{k+1} and S of the next step exactly as warp 0 forms them below
             const double cn = __dsub_rn(s_cm[0], __dmul_rn(rho, __dsub_rn(block_total(3), s_cm[1])));
@@ -395,7 +559,7 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
             const double mu3 = block_total(3);
             const double cn = __dsub_rn(c, __dmul_rn(rho, __dsub_rn(mu3, mu3p)));   // eq-discrete_mass_balance
             bool go = true;
-            if (s_bad) { status = ST_NEG; go = false; }
+            if (block_total(4) > 0.0) { status = ST_NEG; go = false; }
             else if (cn < 0.0) { status = ST_INFEAS; go = false; }
             else {
                 c = cn; mu3p = mu3;
@@ -404,16 +568,18 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                 if (sample) {
                     const double mu0 = block_total(0), mu1 = block_total(1), mu2 = block_total(2);
                     if (lane == 0) {
-                        double* r = kp.rec + ((size_t)s * kp.M + m) * 6;
-                        r[0] = t; r[1] = c; r[2] = mu0; r[3] = mu1; r[4] = mu2; r[5] = mu3;
                         const double Lb = mu1 / mu0;
                         const double rc = (c - tgt[2 * m]) / rms_c, rL = (Lb - tgt[2 * m + 1]) / rms_L;
                         loss += rc * rc + rL * rL;
-                        const double gL = 2.0 * rL / rms_L;                 // d loss / d Lbar
-                        double* tr = trs + (size_t)k * ADJ_TR;
-                        tr[TR_LC] = 2.0 * rc / rms_c;
-                        tr[TR_L0] = -gL * mu1 / (mu0 * mu0);
-                        tr[TR_L1] = gL / mu0;
+                        if (rank == 0) {
+                            double* r = kp.rec + ((size_t)s * kp.M + m) * 6;
+                            r[0] = t; r[1] = c; r[2] = mu0; r[3] = mu1; r[4] = mu2; r[5] = mu3;
+                            const double gL = 2.0 * rL / rms_L;             // d loss / d Lbar
+                            double* tr = trs + (size_t)k * ADJ_TR;
+                            tr[TR_LC] = 2.0 * rc / rms_c;
+                            tr[TR_L0] = -gL * mu1 / (mu0 * mu0);
+                            tr[TR_L1] = gL / mu0;
+                        }
                     }
                 }
                 if (landing) { ++m; if (m < kp.M) tn_c = kp.t_samples[m]; }
@@ -437,14 +603,18 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     PBE_ATS(tf1);
     PBE_ATA(0, tf0, tf1);
     if (warp == 0 && lane == 0) {
-        kp.status[s] = status;
-        kp.steps[s] = nstep;
-        kp.loss[s] = status == ST_OK ? loss : __longlong_as_double(0x7ff8000000000000ll);
+        if (rank == 0) {
+            kp.status[s] = status;
+            kp.steps[s] = nstep;
+            kp.loss[s] = status == ST_OK ? loss : __longlong_as_double(0x7ff8000000000000ll);
+        }
         s_ok = status == ST_OK;
     }
-    __syncthreads();
+    if constexpr (CL) __threadfence();                     // trace, records, trajectory rows -> cluster
+    cl_sync();                                             // (CL: no CTA leaves while others read its smem)
     if (!s_ok) {
-        for (int j = tid; j < kp.n_params; j += NT) ap.gtheta[(size_t)s * kp.n_params + j] = __longlong_as_double(0x7ff8000000000000ll);
+        if (rank == 0)
+            for (int j = tid; j < kp.n_params; j += NT) ap.gtheta[(size_t)s * kp.n_params + j] = __longlong_as_double(0x7ff8000000000000ll);
         return;
     }
     const long long Ktot = s_nsteps;
@@ -468,7 +638,7 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     const long long nseg = (Ktot + Kseg - 1) / Kseg;
     if (ap.traj && Ktot > 0) {                             // n^K and n^{K-1} before the first step
         __syncthreads();                                   // the final state's global stores are done
-        __threadfence_block();
+        __threadfence_block();                             // (CL: fenced + cluster-synced above)
         fetch_state(Ktot);
         fetch_state(Ktot - 1);
         cp_async_commit_wait_all();
@@ -573,12 +743,17 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                 else          v += Lf[e + 1] * wlo[e + 1] + Lf[e] * wmid[e] + Lf[e - 1] * whi[e - 1];
                 lout[PX(kq + 2)] = v;
             }
+            push_halo(lout, (int)(kk & 1));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) lamC += __shfl_xor_sync(0xffffffffu, lamC, off);
-            if (lane == 0) s_red[warp][0] = lamC;
+            {
+                const double a[5] = {lamC, 0.0, 0.0, 0.0, 0.0};
+                put_partials((int)(kk & 1), a);
+            }
             PBE_ATS(tv3);
             PBE_ATA(11, tv2, tv3);
-            __syncthreads();
+            exchange((int)(kk & 1), true);
+            rpar = (int)(kk & 1);
             PBE_ATS(tb1);
             PBE_ATA(2, tb0, tb1);
             // ---- scalar phase (warp 0): adjoints of c^kk, t^kk, mu3p^kk; lambda_G^kk ------------
@@ -591,7 +766,7 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                 const double lG = LC * r[TR_CG] + lam_t * r[TR_TG];
                 lam_mu = rho * lcp;
                 lam_c = nc; lam_t = nt;
-                if (lane == 0) trs[(size_t)kk * ADJ_TR + TR_LG] = lG;
+                if (lane == 0 && rank == 0) trs[(size_t)kk * ADJ_TR + TR_LG] = lG;
                 if (kk > k0) pre_step(kk - 1);
             }
             if (ap.traj) asm volatile("cp.async.wait_group 0;" ::: "memory");   // n^{kk-1}: this thread's part
@@ -602,6 +777,7 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         }
         __syncthreads();
     }
+    if constexpr (CL) cg::this_cluster().sync();          // no CTA leaves while others read its smem
 #if PBE_TIMING
     if (blockIdx.x == 0 && tid == 0) { t_acc[4] = (unsigned long long)Ktot; for (int i = 0; i < 16; ++i) g_adj_cycles[i] = t_acc[i]; }
 #endif

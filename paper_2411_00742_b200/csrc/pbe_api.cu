@@ -629,6 +629,11 @@ const AdjointVariant kAdjoint[] = {
     {4, 512, (const void*)&pbe::k_adjoint<4, 512>},   // PBE_ADJ_K=4 A/B only (N = 2000: 99 vs 87 ms)
     {16, 256, (const void*)&pbe::k_adjoint<16>}, {24, 256, (const void*)&pbe::k_adjoint<24>},
 };
+// cluster variants (trajectory mode): 64 threads x K bins per CTA, CS CTAs per simulation
+const AdjointVariant kAdjointCL[] = {
+    {2, 64, (const void*)&pbe::k_adjoint<2, 64, true>}, {4, 64, (const void*)&pbe::k_adjoint<4, 64, true>},
+    {8, 64, (const void*)&pbe::k_adjoint<8, 64, true>},
+};
 
 // ------------------------------------------------------------------------------------
 // C ABI
@@ -1020,17 +1025,42 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     }
     if (!av) return fail(ctx, PBE_ERR_ARG, "pbe_run_adjoint: N = %d exceeds the adjoint kernel (N <= 6144)", N);
     const long long ms = cf.max_steps;
+    // trajectory mode (checkpoint_every = 0): every state in HBM when it takes <= 16 GB (NEXT-3:
+    // 9 x 12,001 x 2000 doubles = 1.7 GB) -- no re-march in the reverse pass; else O(sqrt) checkpoints
+    const bool traj_mem = checkpoint_every == 0 &&
+                          (double)n_sims * (ms + 1) * N * sizeof(double) <= 16.0 * (1ull << 30) &&
+                          !getenv("PBE_ADJ_RECOMPUTE");
+    // cluster mode (trajectory only): CS CTAs per simulation when the batch leaves SMs idle and the
+    // mesh is large enough for the per-step latency to be the vector phases' (N >= 1024);
+    // PBE_ADJ_CLUSTER = 0 disables it, = CS forces CS
+    int cs = 1;
+    {
+        const char* e = getenv("PBE_ADJ_CLUSTER");
+        const int want = e ? atoi(e) : -1;
+        int sms = 0;
+        CUDA_TRY(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        if (traj_mem && want != 0 && (want > 0 || N >= 1024)) {
+            for (int c : {16, 8, 4, 2}) {
+                if (want > 0 && c != want) continue;
+                if (want < 0 && n_sims * c > sms) continue;
+                for (const auto& v : kAdjointCL) {
+                    const int nb = 64 * v.K;          // bins per CTA; every CTA but the last is full
+                    if (c * nb >= N && (c - 1) * nb < N) {
+                        av = &v; cs = c; nt = 64;
+                        smem = (size_t)4 * pbe::adj_row(64, v.K) * sizeof(double);
+                        break;
+                    }
+                }
+                if (cs > 1) break;
+            }
+        }
+    }
     // segment length: the segment's trace rows are staged in shared memory every segment, and
     // its states n^{k0..k1} live there too when they fit (else in a global buffer)
     const size_t smem_cap = 220 * 1024, row = (size_t)pbe::adj_row(nt, av->K) * sizeof(double), trow = pbe::ADJ_TR * sizeof(double);
     int Kseg = checkpoint_every;
-    // checkpoint_every = 0 (auto): keep the whole trajectory in HBM when it takes <= 16 GB (C5-size
-    // NEXT-3: 9 x 12,001 x 2000 doubles = 1.7 GB) -- no re-march in the reverse pass; else O(sqrt)
     const int NRr = (N + 1) & ~1;
-    const bool traj = checkpoint_every == 0 &&
-                      (double)n_sims * (ms + 1) * N * sizeof(double) <= 16.0 * (1ull << 30) &&
-                      smem + 3 * row + 64 * (size_t)pbe::ADJ_TR * sizeof(double) <= 220 * 1024 &&
-                      !getenv("PBE_ADJ_RECOMPUTE");
+    const bool traj = traj_mem && smem + 3 * row + 64 * (size_t)pbe::ADJ_TR * sizeof(double) <= 220 * 1024;
     if (Kseg == 0) Kseg = std::max(8, (int)std::ceil(std::sqrt((double)ms)));       // O(sqrt) memory
     int seg_smem = 0;
     if (traj) {
@@ -1074,7 +1104,24 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     ctx->info = pbe_run_info{};
     void* args[] = {&ap};
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    CUDA_TRY(ctx, cudaLaunchKernel(av->fn, dim3(n_sims), dim3(nt), args, smem, st));
+    if (cs > 1) {
+        if (cs > 8) CUDA_TRY(ctx, cudaFuncSetAttribute(av->fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(n_sims * cs);
+        lc.blockDim = dim3(nt);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        CUDA_TRY(ctx, cudaLaunchKernelExC(&lc, av->fn, args));
+    } else {
+        CUDA_TRY(ctx, cudaLaunchKernel(av->fn, dim3(n_sims), dim3(nt), args, smem, st));
+    }
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->n_params > 0) {
         pbe::k_adjoint_theta<<<dim3((ctx->n_params + 31) / 32, n_sims), 256, 0, st>>>(ap);
@@ -1084,8 +1131,8 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
     ctx->info.kernel = PBE_KERNEL_ADJOINT;
     ctx->info.launches = ctx->n_params > 0 ? 2 : 1;
     ctx->info.threads_per_cta = nt;
-    ctx->info.ctas = n_sims;
-    ctx->info.cluster = 1;
+    ctx->info.ctas = n_sims * cs;
+    ctx->info.cluster = cs;
     ctx->info.bins_per_thread = av->K;
     ctx->info.steps_per_pass = 1;
     ctx->info.main_ms = -1.0;

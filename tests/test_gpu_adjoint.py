@@ -224,3 +224,53 @@ def test_adjoint_dissolution_outflow_at_zero(N):
     w = W.replace(w, N=N, dL=dL, n0=W.gaussian_seed(N, dL, mean=60.0, sigma=40.0, m0=0.5)[None, :], c0=c0,
                   t_samples=t, dt_max=0.5, target=W._target(c0, t), max_steps=20000)
     _check(w)
+
+
+# ---- cluster mode (k_adjoint<K, 64, true>: CS CTAs per simulation, DSMEM halos) -------------------
+@pytest.mark.parametrize("cs,N", [(2, 200), (4, 450), (8, 1000), (16, 2000), (16, 1950)])
+def test_adjoint_cluster_matches_oracle(cs, N, monkeypatch):
+    """The cluster variant forced at CS = 2..16 (bins split over CTAs, edge values pushed into the
+    neighbours' ghost cells, partial sums added across the cluster) against the oracle."""
+    monkeypatch.setenv("PBE_ADJ_CLUSTER", str(cs))
+    w = small_ensemble(n_sims=3, N=N, t_max=20.0, M=6)
+    lo, go = oracle_grad(w)
+    g, rec, info = gpu_adjoint(w)
+    assert info["cluster"] == cs, info
+    assert (rec["status"] == 0).all(), rec["status"]
+    assert np.all(np.abs(g["loss"] - lo) <= RTOL_LOSS * np.abs(lo)), (g["loss"], lo)
+    err = np.abs(g["grad"] - go) / np.max(np.abs(go), axis=1, keepdims=True)
+    assert err.max() <= RTOL_GRAD, f"max grad err {err.max():.3e}"
+
+
+@pytest.mark.parametrize("cs,N", [(2, 129), (2, 256)])
+def test_adjoint_cluster_outflow_and_dissolution(cs, N, monkeypatch):
+    """Cluster mode with mass at the outflow face (last CTA partial or full) and with dissolution
+    (C < 0: the sweep runs the other way across the CTA boundary)."""
+    monkeypatch.setenv("PBE_ADJ_CLUSTER", str(cs))
+    w = small_ensemble(n_sims=2, N=N, t_max=20.0, M=5)
+    w = W.replace(w, n0=W.gaussian_seed(N, 1200.0 / N, mean=1100.0, sigma=70.0)[None, :])
+    _check(w)
+    wd = W.c2_dissolution()
+    dL = 1200.0 / N
+    t = np.linspace(3.0, 30.0, 10)
+    c0 = np.array([4.0])
+    wd = W.replace(wd, N=N, dL=dL, n0=W.gaussian_seed(N, dL, mean=60.0, sigma=40.0, m0=0.5)[None, :], c0=c0,
+                   t_samples=t, dt_max=0.5, target=W._target(c0, t), max_steps=20000)
+    _check(wd)
+
+
+def test_adjoint_cluster_failed_simulation_gives_nan(monkeypatch):
+    monkeypatch.setenv("PBE_ADJ_CLUSTER", "2")
+    w = W.replace(small_ensemble(n_sims=2), max_steps=50)
+    g, rec, info = gpu_adjoint(w)
+    assert info["cluster"] == 2
+    assert (rec["status"] == 5).all()
+    assert np.isnan(g["grad"]).all() and np.isnan(g["loss"]).all()
+
+
+def test_adjoint_cluster_is_the_default_for_next3():
+    """NEXT-3 (9 experiments, N = 2000) runs 16-CTA clusters (144 SMs) by default."""
+    w = W.next3_estimation(n_params=40, t_max=30.0, M=30)
+    g, rec, info = gpu_adjoint(w)
+    assert info["cluster"] == 16 and info["ctas"] == 144, info
+    assert (rec["status"] == 0).all()

@@ -338,6 +338,20 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         }
         return t;
     };
+    // two slots at once (one butterfly): sums of slots m1 and m2
+    auto red_total2 = [&](int m1, int m2, int par, double& t1, double& t2) __attribute__((always_inline)) {
+        t1 = 0.0; t2 = 0.0;
+        if constexpr (!CL) {
+            for (int w = 0; w < NW; ++w) { t1 += s_red[par][w][m1]; t2 += s_red[par][w][m2]; }
+        } else {
+            for (int e = lane; e < CS * NW; e += 32) { t1 += s_red[par][e][m1]; t2 += s_red[par][e][m2]; }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                t1 += __shfl_xor_sync(0xffffffffu, t1, off);
+                t2 += __shfl_xor_sync(0xffffffffu, t2, off);
+            }
+        }
+    };
     int rpar = 0;                                   // parity of the partials being read
     auto block_total = [&](int m) -> double { return red_total(m, rpar, false); };
     // forward update nb[q] -> nb[q^1] (eq-highRes_growth, flux form; clip marks as -0.0)
@@ -545,9 +559,14 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         PBE_ATA(5, tq0, tq1);
         exchange(par, true);
         rpar = par;
+        PBE_ATS(tqx);
+        PBE_ATA(1, tq1, tqx);
+        // mu3(n^{k+1}) and the clip-failure flag in one reduction, by every warp (poly) or warp 0
+        double mu3_k = 0.0, bad_k = 0.0;
+        if (poly_blk || warp == 0) red_total2(3, 4, rpar, mu3_k, bad_k);
         if (poly_blk) {
             // every warp: c^{k+1} and S of the next step exactly as warp 0 forms them below
-            const double cn = __dsub_rn(s_cm[0], __dmul_rn(rho, __dsub_rn(block_total(3), s_cm[1])));
+            const double cn = __dsub_rn(s_cm[0], __dmul_rn(rho, __dsub_rn(mu3_k, s_cm[1])));
             poly_partials(__dmul_rn(cn, KC.ics.v));
             __syncthreads();
             use_blk = true;
@@ -556,10 +575,10 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         PBE_ATA(6, tq1, tq2);
         if (warp == 0) {
             const bool sample = s_sample != 0;
-            const double mu3 = block_total(3);
+            const double mu3 = mu3_k;
             const double cn = __dsub_rn(c, __dmul_rn(rho, __dsub_rn(mu3, mu3p)));   // eq-discrete_mass_balance
             bool go = true;
-            if (block_total(4) > 0.0) { status = ST_NEG; go = false; }
+            if (bad_k > 0.0) { status = ST_NEG; go = false; }
             else if (cn < 0.0) { status = ST_INFEAS; go = false; }
             else {
                 c = cn; mu3p = mu3;
@@ -583,9 +602,13 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                     }
                 }
                 if (landing) { ++m; if (m < kp.M) tn_c = kp.t_samples[m]; }
+                PBE_ATS(tk0);
+                PBE_ATA(12, tq2, tk0);
                 if (m >= kp.M) go = false;
                 else if (nstep >= kp.max_steps) { status = ST_MAXSTEPS; go = false; }
                 else go = kinetics(k + 1);
+                PBE_ATS(tk1);
+                PBE_ATA(13, tk0, tk1);
             }
             if (lane == 0) { s_go = go; s_sample = go && landing; s_nsteps = nstep; s_cm[0] = c; s_cm[1] = mu3p; }
         }
@@ -679,7 +702,6 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
             PBE_ATS(tb0);
             // ---- vector phase: lambda^{kk+1} (+ mass-balance and sample terms, clip marks) ->
             //      lambda^kk, partial lambda_C -------------------------------------------------
-            if (ap.traj && kk >= 1) { fetch_state(kk - 1); cp_async_commit(); }   // lands while we work
             PBE_ATS(tv0);
             PBE_ATA(8, tb0, tv0);
             const double C = s_sc[SC_C], kap2 = s_sc[SC_KAP2], beta2 = s_sc[SC_BETA2];
@@ -703,6 +725,9 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                 }
                 lam[j] = (in && !clipped) ? l : 0.0;
             }
+            // prefetch n^{kk-1} into the free ring slot (after this step's window loads, so the
+            // copies do not queue in front of them); lands while we work
+            if (ap.traj && kk >= 1) { fetch_state(kk - 1); cp_async_commit(); }
             PBE_ATS(tv1);
             PBE_ATA(9, tv0, tv1);
             // face partials (as k_resident's tangent lanes): faces f = i0 - 1 + e, e = 0..K+2

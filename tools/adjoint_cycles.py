@@ -23,9 +23,11 @@ assert lib.pbe_debug_adjoint_cycles(buf) == 0
 c = np.array(buf[:16], dtype=np.float64)
 steps = c[4]
 print(f"params {P}: {ctx.last_run_info()['main_ms']:.1f} ms, {steps:.0f} steps")
-for n, v in zip(["forward", "recompute", "backward vector", "backward scalar"], c[:4]):
+for n, v in zip(["forward", "fwd exchange wait (traj: no recompute)", "backward vector", "backward scalar"], c[:4]):
     print(f"  {n:16s} {v / steps:8.0f} cycles/step")
 for n, v in zip(["fwd update+moments", "fwd barrier+poly", "fwd warp-0 chain"], c[5:8]):
     print(f"    {n:18s} {v / steps:8.0f} cycles/step")
 for n, v in zip(["bwd theta", "bwd loads", "bwd faces", "bwd out+shfl"], c[8:12]):
+    print(f"    {n:18s} {v / steps:8.0f} cycles/step")
+for n, v in zip(["chain pre-kinetics", "chain kinetics"], c[12:14]):
     print(f"    {n:18s} {v / steps:8.0f} cycles/step")

@@ -493,6 +493,7 @@ def main():
             g3 = ctx3.adjoint_gradient(P3)
             torch.cuda.synchronize(); ta.append(time.perf_counter() - t0)
         r3 = ctx3.moments()
+        i3 = ctx3.last_run_info()
         ctx3.close()
         h = 1e-6
         th = np.repeat(w3.theta, P3 + 1, axis=0)
@@ -511,7 +512,9 @@ def main():
                               f"{int(r3['steps'].max())} steps", metric="ms per gradient (wall, incl. copies)",
                      adjoint_ms=1e3 * min(ta), fd_batched_ms=1e3 * tf, fd_sims=int(wf.n_sims),
                      speedup_vs_fd=tf / min(ta), finite=bool(np.isfinite(g3["grad"]).all()),
-                     note="forward-mode tangents need 100 passes of 10 lanes (tools/next3_time.py: 205x slower)")
+                     kernel_ms=i3["main_ms"], cluster=i3["cluster"], ctas=i3["ctas"],
+                     note="k_adjoint in 16-CTA clusters (one per experiment) + k_adjoint_theta; forward-mode "
+                          "tangents need 100 passes of 10 lanes (tools/next3_time.py: ~400x slower)")
         del n03
 
     # ---- strong scaling on one GPU: the rank-0 shard of W = 2, 4, 8 GPUs (BASELINE config 5 as written) --

@@ -18,7 +18,8 @@ LIMITS = {
     "_ZN3pbe10k_2d_fusedENS_9Params2DFE": 96,                             # NEXT-1
     "_ZN3pbe11k_stream_tbENS_14StreamTBParamsE": 256,                     # NEXT-4 (C4 default)
     "_ZN3pbe8k_streamILi0ELb1EEEvNS_12StreamParamsE": 160,                # C4 plain streaming (dynamic tiles)
-    "_ZN3pbe9k_adjointILi8EEEvNS_9AdjParamsE": 64,                        # NEXT-3
+    "_ZN3pbe9k_adjointILi2ELi64ELb1EEEvNS_9AdjParamsE": 64,              # NEXT-3 (16-CTA clusters)
+    "_ZN3pbe9k_adjointILi8ELi256ELb0EEEvNS_9AdjParamsE": 64,             # NEXT-3 single-CTA (PBE_ADJ_CLUSTER=0)
 }
 
 

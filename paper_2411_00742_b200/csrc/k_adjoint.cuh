@@ -453,7 +453,17 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
                 dq = fma(dq, x, qv);
                 qv = fma(qv, x, pc[i]);
             }
-            const double xl = ipow(x, j0);
+            // x^(tid PM) = (x^PM)^tid: the PM-power by squarings (PM a power of two), then the
+            // thread-dependent part -- the same products as ipow(x, tid PM), fewer loop trips
+            double xl;
+            if constexpr ((PM & (PM - 1)) == 0) {
+                double xp = x;
+#pragma unroll
+                for (int m = 1; m < PM; m <<= 1) xp = xp * xp;
+                xl = tid > 0 ? ipow(xp, tid) : 1.0;
+            } else {
+                xl = ipow(x, j0);
+            }
             tt = xl * x * qv;
             dtt = xl * fma((double)(j0 + 1), qv, x * dq);
         } else if (Sv > 1.0) {
@@ -564,10 +574,14 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         // mu3(n^{k+1}) and the clip-failure flag in one reduction, by every warp (poly) or warp 0
         double mu3_k = 0.0, bad_k = 0.0;
         if (poly_blk || warp == 0) red_total2(3, 4, rpar, mu3_k, bad_k);
+        PBE_ATS(tp0);
+        PBE_ATA(14, tqx, tp0);
         if (poly_blk) {
             // every warp: c^{k+1} and S of the next step exactly as warp 0 forms them below
             const double cn = __dsub_rn(s_cm[0], __dmul_rn(rho, __dsub_rn(mu3_k, s_cm[1])));
             poly_partials(__dmul_rn(cn, KC.ics.v));
+            PBE_ATS(tp1);
+            PBE_ATA(15, tp0, tp1);
             __syncthreads();
             use_blk = true;
         }

@@ -192,11 +192,15 @@ __device__ __forceinline__ D1 growth_rate(const KParams& kp, const LD& L, D1 S, 
 // x^e for an integer e >= 0 by binary exponentiation (<= 2 log2(e) multiplications instead of
 // pow()'s exp/log: the long-polynomial chunk offsets and the adjoint's d G / d a_j = x^(j+1)).
 __device__ __forceinline__ double ipow(double x, int e) {
+    // binary exponentiation with a select instead of a branch per bit (lanes of a warp take
+    // different exponents; a divergent branch per bit cost ~50 cycles per iteration): the same
+    // products in the same order as the branchy form, so bitwise the same result
     double r = 1.0, b = x;
     while (e > 0) {
-        if (e & 1) r *= b;
+        const double rb = r * b;
+        r = (e & 1) ? rb : r;
         e >>= 1;
-        if (e) b *= b;
+        b = e ? b * b : b;
     }
     return r;
 }

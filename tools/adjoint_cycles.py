@@ -31,3 +31,5 @@ for n, v in zip(["bwd theta", "bwd loads", "bwd faces", "bwd out+shfl"], c[8:12]
     print(f"    {n:18s} {v / steps:8.0f} cycles/step")
 for n, v in zip(["chain pre-kinetics", "chain kinetics"], c[12:14]):
     print(f"    {n:18s} {v / steps:8.0f} cycles/step")
+for n, v in zip(["poly: reduction", "poly: partials"], c[14:16]):
+    print(f"    {n:18s} {v / steps:8.0f} cycles/step")

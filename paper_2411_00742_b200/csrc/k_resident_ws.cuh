@@ -162,6 +162,11 @@ __device__ __forceinline__ void ws_tangent_sweep(double (&x)[PG][KT], const doub
         const int lo = NEG ? f - 1 : f - 2;
         return fma(wh, X(p, lo + 2, o), fma(wm, X(p, lo + 1, o), wl * X(p, lo, o)));
     };
+    // Stencil form of the flux update (per lane 1 DMUL + 3 DFMA instead of the flux form's
+    // 3 + 2): with F_f = wl_f y_lo + wm_f y_mid + wh_f y_hi, bin k's update y_k - (F_{k+1} - F_k)
+    // regroups into four per-bin coefficients shared by all lanes.  The sweep runs in place in
+    // the primal's order, so the neighbour already updated is carried as its old value (yo).
+#if PBE_WS_FLUXFORM
     double Fc[PG > 0 ? PG : 1];
     if (!NEG) {
         {
@@ -198,6 +203,51 @@ __device__ __forceinline__ void ws_tangent_sweep(double (&x)[PG][KT], const doub
             }
         }
     }
+#else
+    (void)Ft;
+    double yo[PG > 0 ? PG : 1];
+    if (!NEG) {
+        // C >= 0, right to left: F_f touches (f-2, f-1, f);
+        // y_k' = (1 - wm_{k+1} + wh_k) y_k + (wm_k - wl_{k+1}) y_{k-1} + wl_k y_{k-2} - wh_{k+1} y_{k+1}
+        double wlR = wlo[KT * NTG + tt], whR = whi[KT * NTG + tt];
+        double wmR = C - (wlR + whR);
+#pragma unroll
+        for (int p = P0; p < P1; ++p) yo[p] = X(p, KT, 0);         // old y_{k+1} (halo)
+#pragma unroll
+        for (int k = KT - 1; k >= 0; --k) {
+            const int o = (LAG > 0 && k + LAG < KT) ? ws_order(x[P0][k + LAG < KT ? k + LAG : 0]) : 0;
+            const double wl = wlo[k * NTG + tt + o], wh = whi[k * NTG + tt + o], wm = C - (wl + wh);
+            const double c0 = (1.0 - wmR) + wh, c1 = wm - wlR;
+#pragma unroll
+            for (int p = P0; p < P1; ++p) {
+                const double y = x[p][k];
+                x[p][k] = fma(c0, y, fma(c1, X(p, k - 1, o), fma(wl, X(p, k - 2, o), -whR * yo[p])));
+                yo[p] = y;
+            }
+            wlR = wl; whR = wh; wmR = wm;
+        }
+    } else {
+        // C < 0, left to right: F_f touches (f-1, f, f+1);
+        // y_k' = (1 - wl_{k+1} + wm_k) y_k + (wh_k - wm_{k+1}) y_{k+1} - wh_{k+1} y_{k+2} + wl_k y_{k-1}
+        double wlL = wlo[tt], whL = whi[tt];
+        double wmL = C - (wlL + whL);
+#pragma unroll
+        for (int p = P0; p < P1; ++p) yo[p] = X(p, -1, 0);         // old y_{k-1} (halo)
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+            const int o = (LAG > 0 && k >= LAG) ? ws_order(x[P0][k >= LAG ? k - LAG : 0]) : 0;
+            const double wl = wlo[(k + 1) * NTG + tt + o], wh = whi[(k + 1) * NTG + tt + o], wm = C - (wl + wh);
+            const double c0 = (1.0 - wl) + wmL, c1 = whL - wm;
+#pragma unroll
+            for (int p = P0; p < P1; ++p) {
+                const double y = x[p][k];
+                x[p][k] = fma(c0, y, fma(c1, X(p, k + 1, o), fma(wlL, yo[p], -wh * X(p, k + 2, o))));
+                yo[p] = y;
+            }
+            wlL = wl; whL = wh; wmL = wm;
+        }
+    }
+#endif
 }
 
 #if PBE_TIMING

@@ -100,13 +100,17 @@ def replicate_single(w, world: int):
 #       F = C n_up + kappa psi (2), update (2), mu3 (1), clip test (1)
 #   tangent support per face 10: b r, a r (2), qa, qb (2), kappa qa, kappa qb (2),
 #       g = n_up + beta psi (1), dg (1), w_mid (2)
-#   per tangent lane 7: lane flux (3), update (2), Cdot dg (1), mu3dot (1)
+#   per tangent lane 7: lane flux (3), update (2), Cdot dg (1), mu3dot (1)   [k_resident: flux form]
+#   k_resident_ws (stencil form of the same update): per bin 3 (two coefficient sums), per lane 6:
+#       stencil (1 DMUL + 3 DFMA), Cdot dg (1), mu3dot (1)
 #   upwind: primal 6 (F 1, update 2, mu3 1, clip 1, n_up 1), lane 5 (flux 1, update 2, Cdot 1, mu3dot 1)
 # SURVEY §8(d) estimated ~19 + 10 per lane before the kernels existed; the counts above are
 # the implemented formulation's (its SASS executes 91.5 for C5: profiles/fp64_instr.json).
-def fp64_instr_per_bin_update(limiter: int, P: int) -> float:
+def fp64_instr_per_bin_update(limiter: int, P: int, stencil: bool = False) -> float:
     if limiter == W.LIM_UPWIND:
         return 6.0 + (1.0 if P else 0.0) + 5.0 * P
+    if stencil and P:
+        return 15.0 + 10.0 + 3.0 + 6.0 * P
     return 15.0 + (10.0 if P else 0.0) + 7.0 * P
 
 
@@ -334,7 +338,7 @@ def main():
                      kernel=kname, bytes_per_bin_update=bytes_per,
                      peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s", kernel_ms=kms)
         else:
-            f = fp64_instr_per_bin_update(w.limiter, P)
+            f = fp64_instr_per_bin_update(w.limiter, P, stencil=bool(info.get("warp_specialized")))
             achieved = f * bu_local / (kms * 1e-3) / 1e12
             sm_max = float(peaks.get("sm_max_mhz", 1965.0))
             nominal = 148 * 64 * sm_max * 1e6 / 1e12      # FP64 lanes x SMs x max SM clock (instr/s)

@@ -1046,6 +1046,23 @@ pbe_status pbe_run_adjoint(pbe_ctx ctx, int32_t n_sims, const double* n0, int64_
                 for (const auto& v : kAdjointCL) {
                     const int nb = 64 * v.K;          // bins per CTA; every CTA but the last is full
                     if (c * nb >= N && (c - 1) * nb < N) {
+                        // the cluster shape must be schedulable on this device (16 is non-portable)
+                        if (c > 8) cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                        cudaLaunchConfig_t oc{};
+                        oc.gridDim = dim3(c);
+                        oc.blockDim = dim3(64);
+                        oc.dynamicSmemBytes = (size_t)4 * pbe::adj_row(64, v.K) * sizeof(double) +
+                                              64 * (size_t)pbe::ADJ_TR * sizeof(double);
+                        cudaLaunchAttribute oa[1];
+                        oa[0].id = cudaLaunchAttributeClusterDimension;
+                        oa[0].val.clusterDim.x = c; oa[0].val.clusterDim.y = 1; oa[0].val.clusterDim.z = 1;
+                        oc.attrs = oa;
+                        oc.numAttrs = 1;
+                        int ncl = 0;
+                        if (cudaOccupancyMaxActiveClusters(&ncl, v.fn, &oc) != cudaSuccess || ncl < 1) {
+                            cudaGetLastError();
+                            break;
+                        }
                         av = &v; cs = c; nt = 64;
                         smem = (size_t)4 * pbe::adj_row(64, v.K) * sizeof(double);
                         break;

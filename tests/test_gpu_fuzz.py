@@ -175,3 +175,42 @@ def test_fuzz_adjoint_matches_oracle(seed):
     assert np.all(np.abs(g["loss"][ok] - lo[ok]) <= RTOL_LOSS * np.abs(lo[ok]))
     scale = np.max(np.abs(go[ok]), axis=1, keepdims=True)
     assert (np.abs(g["grad"][ok] - go[ok]) / np.maximum(scale, 1e-300)).max() <= RTOL_GRAD
+
+
+def _cluster_size_for(N):
+    """The CS in {16, 8, 4, 2} for which libpbe's cluster adjoint (64 threads x K in {2, 4, 8} bins
+    per CTA, every CTA but the last full) takes N, or 0."""
+    for c in (16, 8, 4, 2):
+        for K in (2, 4, 8):
+            nb = 64 * K
+            if c * nb >= N and (c - 1) * nb < N:
+                return c
+    return 0
+
+
+@pytest.mark.parametrize("seed", range(max(8, NF // 5)))
+def test_fuzz_adjoint_cluster_matches_oracle(seed, monkeypatch):
+    """The cluster adjoint (CTAs exchanging halos and partials with st.async) on random cases."""
+    from tests.test_gpu_adjoint import RTOL_GRAD, RTOL_LOSS, gpu_adjoint, oracle_grad
+    rng = np.random.Generator(np.random.PCG64(9500 + seed))
+    w, _ = random_case(seed + 100)
+    if w.n_steps:
+        w = W.replace(w, n_steps=0, t_samples=np.linspace(2.0, 2.0 * int(rng.integers(2, 7)), int(rng.integers(1, 6))))
+    N = int(rng.integers(129, 1025))
+    cs = _cluster_size_for(N)
+    if cs == 0:
+        N, cs = 200, 2
+    w = W.replace(w, N=N, dL=1200.0 / N, n0=W.gaussian_seed(N, 1200.0 / N, mean=float(rng.uniform(300, 900)))[None, :],
+                  n_tangents=0, tangent_seed=None, target=W._target(w.c0, w.t_samples))
+    monkeypatch.setenv("PBE_ADJ_CLUSTER", str(cs))
+    lo, go = oracle_grad(W.replace(w, max_steps=4000), allow_fail=True)
+    ok = np.isfinite(lo)
+    g, rec, info = gpu_adjoint(w)
+    assert info["cluster"] == cs, (N, cs, info)
+    o_status = oracle.run(w, want_n=False)["status"]
+    assert np.array_equal(rec["status"], o_status)
+    if not ok.any():
+        return
+    assert np.all(np.abs(g["loss"][ok] - lo[ok]) <= RTOL_LOSS * np.abs(lo[ok]))
+    scale = np.max(np.abs(go[ok]), axis=1, keepdims=True)
+    assert (np.abs(g["grad"][ok] - go[ok]) / np.maximum(scale, 1e-300)).max() <= RTOL_GRAD

@@ -203,11 +203,10 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
             if (i >= 0 && i < N) cp_async8(dst + x + x / K, src + i);
         }
     };
-    // warp partials, double-buffered by step parity: [par][rank NW + warp][m] -- in CL mode every
+    // warp partials, double-buffered by step parity: [par][m][rank NW + warp] -- in CL mode every
     // warp pushes its partials into EVERY CTA of the cluster (remote stores do not stall), so the
-    // reads after the cluster barrier are local
-    // slots: mu0..mu3 (or lambda_C, 0, 0, 0), the warp's clip-failure flag, pad
-    __shared__ __align__(16) double s_red[2][32][6];
+    // reads after the exchange are local; m: mu0..mu3 (or lambda_C, 0, 0, 0), clip-failure flag
+    __shared__ __align__(16) double s_red[2][5][32];
     __shared__ unsigned long long s_mbar[2];       // CL: one mbarrier per parity (partials + halos)
     unsigned mph = 0;                              // CL: phase bit of s_mbar[0], s_mbar[1]
     __shared__ double s_sc[12];
@@ -218,6 +217,7 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     enum { SC_C = 0, SC_KAP2, SC_BETA2, SC_LM, SC_L0, SC_L1, SC_LG, SC_S, SC_T, SC_CLIP };
 
     for (int j = tid; j < 4 * NP; j += NT) sm[j] = 0.0;
+    for (int j = tid; j < 2 * 5 * 32; j += NT) (&s_red[0][0][0])[j] = 0.0;
     if (CL && tid == 0) {
         adj_mbar_init(&s_mbar[0], NW);             // every local warp arrives once per phase
         adj_mbar_init(&s_mbar[1], NW);
@@ -264,19 +264,18 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
     // rank NW + warp of every CTA (lane r stores to rank r; remote ones with st.async)
     auto put_partials = [&](int par, const double* a) __attribute__((always_inline)) {
         if constexpr (CL) {
-            double* d = &s_red[par][rank * NW + warp][0];
+            const int e = rank * NW + warp;
             if (lane == rank) {
 #pragma unroll
-                for (int m = 0; m < 5; ++m) d[m] = a[m];
+                for (int m = 0; m < 5; ++m) s_red[par][m][e] = a[m];
             } else if (lane < CS) {
                 const unsigned rb = adj_mapa(&s_mbar[par], lane);
-                adj_st_async2(adj_mapa(d, lane), a[0], a[1], rb);
-                adj_st_async2(adj_mapa(d + 2, lane), a[2], a[3], rb);
-                adj_st_async2(adj_mapa(d + 4, lane), a[4], 0.0, rb);
+#pragma unroll
+                for (int m = 0; m < 5; ++m) adj_st_async1(adj_mapa(&s_red[par][m][e], lane), a[m], rb);
             }
         } else if (lane == 0) {
 #pragma unroll
-            for (int m = 0; m < 5; ++m) s_red[par][warp][m] = a[m];
+            for (int m = 0; m < 5; ++m) s_red[par][m][warp] = a[m];
         }
     };
     // the exchange point of a step: the partials of parity par (and, with halo, the neighbours'
@@ -286,7 +285,7 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         if constexpr (CL) {
             __syncwarp();
             if (lane == 0) {
-                const unsigned tx = (unsigned)((CS - 1) * NW * 48) +
+                const unsigned tx = (unsigned)((CS - 1) * NW * 40) +
                                     (halo ? 16u * ((rank > 0) + (rank < CS - 1)) : 0u);
                 adj_mbar_arrive(&s_mbar[par], warp == 0 ? tx : 0u);
             }
@@ -318,38 +317,42 @@ __global__ void __launch_bounds__(NTB) k_adjoint(const AdjParams ap) {
         a[4] = __any_sync(0xffffffffu, bad) ? 1.0 : 0.0;
         put_partials(par, a);
     };
-    // total (or max) of slot m of the partials s_red[par] over the CTA -- over the cluster in CL
-    // mode (lane e loads partial e % NW of rank e / NW, then a butterfly: identical in every lane
-    // and every CTA).  Whole warps, after the barrier that follows the partials.
-    auto red_total = [&](int m, int par, bool mx) -> double {
-        double t = 0.0;
-        if constexpr (!CL) {
-            for (int w = 0; w < NW; ++w) t = mx ? fmax(t, s_red[par][w][m]) : t + s_red[par][w][m];
-        } else {
-            for (int e = lane; e < CS * NW; e += 32) {
-                const double v = s_red[par][e][m];
-                t = mx ? fmax(t, v) : t + v;
-            }
+    // CL: the 32 partial slots of a row (unused slots stay 0) summed (or max-ed) by a fixed
+    // pairwise tree in registers; every lane loads the row itself (16-byte broadcast loads), so
+    // no shuffles: identical in every lane and every CTA
+    auto tree32 = [&](const double* row, bool mx) __attribute__((always_inline)) -> double {
+        double v[16];
+        const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double o = __shfl_xor_sync(0xffffffffu, t, off);
-                t = mx ? fmax(t, o) : t + o;
-            }
+        for (int i = 0; i < 16; ++i) {
+            const double2 p2 = r2[i];
+            v[i] = mx ? fmax(p2.x, p2.y) : p2.x + p2.y;
         }
-        return t;
-    };
-    // two slots at once (one butterfly): sums of slots m1 and m2
-    auto red_total2 = [&](int m1, int m2, int par, double& t1, double& t2) __attribute__((always_inline)) {
-        t1 = 0.0; t2 = 0.0;
-        if constexpr (!CL) {
-            for (int w = 0; w < NW; ++w) { t1 += s_red[par][w][m1]; t2 += s_red[par][w][m2]; }
-        } else {
-            for (int e = lane; e < CS * NW; e += 32) { t1 += s_red[par][e][m1]; t2 += s_red[par][e][m2]; }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                t1 += __shfl_xor_sync(0xffffffffu, t1, off);
-                t2 += __shfl_xor_sync(0xffffffffu, t2, off);
-            }
+        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) v[i] = mx ? fmax(v[i], v[i + w]) : v[i] + v[i + w];
+        return v[0];
+    };
+    // total (or max) of slot m of the partials s_red[par] over the CTA (warp order) -- over the
+    // cluster in CL mode.  Whole warps, after the exchange that follows the partials.
+    auto red_total = [&](int m, int par, bool mx) -> double {
+        if constexpr (!CL) {
+            double t = 0.0;
+            for (int w = 0; w < NW; ++w) t = mx ? fmax(t, s_red[par][m][w]) : t + s_red[par][m][w];
+            return t;
+        } else {
+            return tree32(&s_red[par][m][0], mx);
+        }
+    };
+    // sums of slots m1 and m2
+    auto red_total2 = [&](int m1, int m2, int par, double& t1, double& t2) __attribute__((always_inline)) {
+        if constexpr (!CL) {
+            t1 = 0.0; t2 = 0.0;
+            for (int w = 0; w < NW; ++w) { t1 += s_red[par][m1][w]; t2 += s_red[par][m2][w]; }
+        } else {
+            t1 = tree32(&s_red[par][m1][0], false);
+            t2 = tree32(&s_red[par][m2][0], false);
         }
     };
     int rpar = 0;                                   // parity of the partials being read

@@ -2,7 +2,7 @@
 //  pbe_api.cu — host side of libpbe: the C ABI declared in include/pbe.h.
 //  Validation, context-owned device memory, stream-ordered launches, kernel dispatch
 //  by (N, tangent lanes).  No computation of the method happens here: every step of
-//  the march runs in the CUDA kernels (k_resident.cuh incl. its cluster mode, k_stream.cuh,
+//  the march runs in the CUDA kernels (k_resident.cuh incl. its cluster mode, k_resident_ws.cuh, k_stream.cuh,
 //  k_stream_tb.cuh, k_2d_fused.cuh, k_2d.cuh, k_adjoint.cuh).
 // =====================================================================================
 #include <cuda_runtime.h>

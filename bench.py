@@ -204,7 +204,8 @@ def run_reference(args, rank, world):
         tot_bu += bu; tot_s += s
     value = tot_bu / tot_s
     line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
-                ms_per_step=1e3 * tot_s / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+                ms_per_step=1e3 * tot_s / args.steps, higher_is_better=True,
+                scaling=args.scaling if args.workload == "c5" else "weak", vs_baseline=None,
                 dtype="f64", data="synthetic", impl="reference", config=desc,
                 cpu_baseline=dict(value=value, unit=UNIT, cores=th, kind="oracle", sample=sdesc),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0),
